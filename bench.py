@@ -1,0 +1,363 @@
+"""Throughput benchmark of the coded-link hot path (BASELINE.json metric).
+
+Workload (configs[1]): 5G LDPC BG1 k=8448 n=16896 (Z=384), 16-QAM over AWGN,
+20 BP iterations, batch 65,536 codewords per GPU.  One step = one
+Pipeline.run_batch of the chain binary_source -> ldpc5g_encode -> map_bits
+-> awgn -> demap_app -> ldpc5g_decode -> count_errors on one batch of fresh
+synthetic payload (new RngStream per step), all on the GPU.
+
+  python bench.py [--gpus N --steps K --warmup W]            # B200 arm
+  python bench.py --impl reference [...]                      # CPU reference arm
+
+Under torchrun every rank runs its own batches (weak scaling, no data-path
+collective); timing is CUDA events on the launching stream, max over ranks.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+K_INFO, N_TX, M_BITS = 8448, 16896, 4
+METRIC = "decoded info Gbit/s (LDPC BG1, 20 iters) at 1/2/4/8 B200 vs CPU ref; %roofline"
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--batch", type=int, default=65536)
+    p.add_argument("--variant", default="min-sum")
+    p.add_argument("--iters", type=int, default=20)
+    p.add_argument("--ebno", type=float, default=5.0)
+    p.add_argument("--early-stop", action="store_true")
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-exact", action="store_true")
+    return p.parse_args()
+
+
+def _workload(a):
+    return {"workload": f"chain BG1 k={K_INFO} n={N_TX} 16-QAM AWGN {a.ebno} dB, {a.variant}, "
+                        f"{a.iters} iters {'early-stop' if a.early_stop else 'fixed'}",
+            "code": "ldpc5g BG1 Z=384", "k": K_INFO, "n": N_TX, "modulation": "qam16",
+            "batch_per_gpu": a.batch, "num_iter": a.iters, "variant": a.variant,
+            "early_stop": bool(a.early_stop), "ebno_db": a.ebno,
+            "l2": "inputs larger than L2 (fresh 4.4 GB LLR batch per step)"}
+
+
+# ------------------------------------------------------------------ CPU (oracle port)
+def cpu_chain_rate(a, seconds: float, threads: int):
+    """Oracle port of Pipeline.run_batch on the host cores: `threads` workers
+    each decoding batches of 4 codewords (the reference's [B,E] f64 working
+    set limits per-worker batches) until `seconds`."""
+    from oracle import linksim_oracle as O
+
+    O.code(K_INFO, N_TX)  # build tables outside the timed region
+    per = 4
+    stop = time.perf_counter() + seconds
+    done = []
+
+    def worker(w):
+        b = 0
+        n = 0
+        while time.perf_counter() < stop:
+            O.run_batch(K_INFO, N_TX, M_BITS, a.ebno, per, a.seed, ((w + 1) << 32) | (b + 1), a.variant,
+                        a.iters, "app", a.early_stop)
+            b += 1
+            n += per
+        done.append(n)
+
+    t0 = time.perf_counter()
+    with concurrent.futures.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(worker, range(threads)))
+    el = time.perf_counter() - t0
+    cw = sum(done)
+    return cw * K_INFO / el / 1e9, cw, el
+
+
+def run_reference(a, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(max(0, a.warmup) and 1):
+        cpu_chain_rate(a, min(3.0, a.cpu_seconds), threads)
+    total_cw = 0
+    for _ in range(a.steps):
+        v, cw, _ = cpu_chain_rate(a, a.cpu_seconds / max(1, a.steps) + 2.0, threads)
+        vals.append(v)
+        total_cw += cw
+    v = sum(vals) / len(vals)
+    ms = K_INFO * 4 / (v * 1e9) * 1e3 if v else None
+    line = {"metric": METRIC, "value": v, "unit": "Gbit/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64/f32 (reference precision pattern)", "data": "synthetic",
+            "config": _workload(a), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
+                             "sample": f"{total_cw} codewords in batches of 4 per worker thread, "
+                                       f"oracle port of run_batch (numpy + C BP)"},
+            "e2e": {"value": v, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if "Active" in s[3 + j]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(a, rank, world, local_rank):
+    import torch
+
+    import paper_2203_11854_b200 as lb
+    from paper_2203_11854_b200 import _lib as L
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": K_INFO, "n": N_TX,
+                 "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "fast",
+                             "early_stop": bool(a.early_stop)}},
+        "modulation": {"kind": "qam", "bits_per_symbol": M_BITS},
+        "sweep": {"ebno_db": [a.ebno], "batch_size": a.batch}, "seed": a.seed})
+    pipe = lb.Pipeline(cfg)
+    B = a.batch
+    counts = L.zeros((2,), "int64")
+    stream = torch.cuda.current_stream()
+
+    def rng(step):
+        return lb.RngStream(a.seed, ((rank + 1) << 40) | (step + 1))
+
+    dec_events = []
+
+    def step(i, timed):
+        payload, llr = pipe._llr(a.ebno, B, rng(i))
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=a.early_stop, ref_bits=payload,
+                     want_hard=False, counts=counts)
+        if timed:
+            e1.record(stream)
+            dec_events.append((e0, e1))
+
+    for i in range(a.warmup):
+        step(10_000 + i, False)
+    torch.cuda.synchronize()
+    counts.zero_()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        t0.record(stream)
+        for i in range(a.steps):
+            step(i, True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    dec_ms = sum(e0.elapsed_time(e1) for e0, e1 in dec_events)
+    tm = torch.tensor([ms, dec_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms, dec_ms = float(tm[0]), float(tm[1])
+    errs = counts.cpu().tolist()
+    value = world * B * K_INFO * a.steps / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (k_qc_fast): VN-sweep model, SURVEY.md 8d
+    n_full = 68 * 384
+    iters = a.iters
+    bytes_cw = iters * 4 * n_full + 4 * N_TX + (K_INFO + 7) // 8
+    per_launch_ms = dec_ms / a.steps
+    achieved = B * bytes_cw / (per_launch_ms / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random payload per step)",
+            "config": _workload(a),
+            "gpu_launches": 6 * a.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_qc_fast (fused derate+BP+hard+count)",
+                         "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
+                         "kernel_ms_per_launch": per_launch_ms,
+                         "kernel_share_of_step": dec_ms / ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
+            "clocks": clk.summary(),
+            "errors_in_timed_region": {"bit_errors": errs[0], "block_errors": errs[1],
+                                       "blocks": world * B * a.steps}}
+    if not a.no_e2e:
+        line["e2e"] = e2e_chain(a, pipe, rank, world, dist)
+        line["e2e_decode_only"] = e2e_decode(a, pipe, rank, world, dist)
+    if not a.no_exact and rank == 0:
+        line["exact_mode"] = exact_rate(a, pipe)
+    if rank == 0 and world == 1 and not a.no_cpu:
+        v, cw, el = cpu_chain_rate(a, a.cpu_seconds, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": v, "unit": "Gbit/s", "cores": os.cpu_count() or 1, "kind": "port",
+                                "sample": f"{cw} codewords ({el:.1f} s), oracle port of run_batch, "
+                                          f"batches of 4 per worker thread"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def _wall_max(dist, secs):
+    import torch
+
+    if not dist:
+        return secs
+    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def e2e_chain(a, pipe, rank, world, dist, steps=2):
+    """The public API call a user makes (Pipeline.run_batch, sweep.py:347):
+    host numpy (payload, decoded) out every step."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    B = a.batch
+    pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 99))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t = time.perf_counter()
+    for i in range(steps):
+        p, d = pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (500 + i)))
+    torch.cuda.synchronize()
+    el = _wall_max(dist, time.perf_counter() - t)
+    return {"value": world * B * K_INFO * steps / el / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": 0,
+            "d2h_bytes_per_step": 2 * B * K_INFO,
+            "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys"}
+
+
+def e2e_decode(a, pipe, rank, world, dist, steps=2):
+    """Drop-in decoder with HOST buffers: pinned f32 LLRs in, decoded bits out
+    (ldpc5g_decode(llr, code, mode='fast'))."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    B = a.batch
+    _, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, 77))
+    host = torch.empty(llr.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(llr)
+    del llr
+    out = torch.empty((B, K_INFO), dtype=torch.uint8, pin_memory=True)
+    lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(steps):
+        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
+        out.copy_(dec)
+    torch.cuda.synchronize()
+    el = _wall_max(dist, time.perf_counter() - t)
+    return {"value": world * B * K_INFO * steps / el / 1e9, "unit": "Gbit/s",
+            "h2d_bytes_per_step": 4 * B * N_TX, "d2h_bytes_per_step": B * K_INFO,
+            "api": "ldpc5g_decode(pinned host f32 LLRs) -> host bits"}
+
+
+def exact_rate(a, pipe, B=1024):
+    """Throughput of the bit-exact (reference-arithmetic) decoder on a smaller batch."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    _, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, 55))
+    lb.ldpc5g_decode(llr[:64], pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    lb.ldpc5g_decode(llr, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": B * K_INFO / (ms / 1e3) / 1e9, "unit": "Gbit/s", "batch": B,
+            "note": "exact mode = reference arithmetic, bit-identical min-sum"}
+
+
+def main():
+    a = _args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+    run_b200(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,408 @@
+// C-ABI glue: errors, code/graph handles, and the streaming kernels of the
+// chain (source, mapper, AWGN, demapper, encoder, derate, error counting).
+// Decoders live in bp_exact.cu and bp_fast.cu.
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace lsb {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_status(cudaError_t e, const char *where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return LS_ECUDA;
+}
+
+// ------------------------------------------------------------ binary_source
+// One thread per Philox block = 4 uint64 words = 32 payload bits.  Bit j of
+// word w is (w >> (8j+7)) & 1: low uint32 half first, bytes LSB first, each
+// bit the byte's MSB (numpy bounded uint8 draw).
+__global__ void k_binary_source(uint64_t seed, uint64_t sid, int64_t count, uint8_t *__restrict__ bits) {
+  const int64_t nblk = (count + 31) / 32;
+  for (int64_t blk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; blk < nblk;
+       blk += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    philox4x64_10((uint64_t)blk + 1, 0, 0, 0, sid, seed, w);
+    const int64_t base = blk * 32;
+    if (base + 32 <= count && ((reinterpret_cast<uintptr_t>(bits + base) & 15) == 0)) {
+      uint32_t o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint64_t word = w[q / 2];
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v |= (uint32_t)((word >> (8 * (4 * (q % 2) + t) + 7)) & 1) << (8 * t);
+        o[q] = v;
+      }
+      uint4 *dst = reinterpret_cast<uint4 *>(bits + base);
+      dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+      for (int j = 0; j < 32 && base + j < count; ++j)
+        bits[base + j] = (uint8_t)((w[j / 8] >> (8 * (j % 8) + 7)) & 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------ map_bits
+__global__ void k_map_bits(const uint8_t *__restrict__ bits, int64_t nsym, int m,
+                           const float2 *__restrict__ pts, float2 *__restrict__ x) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int lab = 0;
+    for (int t = 0; t < m; ++t) lab = (lab << 1) | (bits[s * m + t] & 1);
+    x[s] = pts[lab];
+  }
+}
+
+// ------------------------------------------------------------ awgn (fast mode)
+// Counter-based: element pair q uses Philox4x32 counter (q, stream lo, stream hi, 0)
+// under key (seed lo, seed hi); Box-Muller gives two complex normals per call.
+__global__ void k_awgn(const float2 *__restrict__ x, int64_t count, float sigma, uint64_t seed,
+                       uint64_t sid, float2 *__restrict__ y) {
+  const int64_t npair = (count + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)sid, (uint32_t)(sid >> 32)),
+                            make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    // uniforms in (0,1] and [0,1)
+    float u0 = ((r.x >> 8) + 1) * (1.0f / 16777216.0f), u1 = (r.y >> 8) * (1.0f / 16777216.0f);
+    float u2 = ((r.z >> 8) + 1) * (1.0f / 16777216.0f), u3 = (r.w >> 8) * (1.0f / 16777216.0f);
+    float rad0 = sqrtf(-2.0f * logf(u0)), rad1 = sqrtf(-2.0f * logf(u2));
+    float s0, c0, s1, c1;
+    sincospif(2.0f * u1, &s0, &c0);
+    sincospif(2.0f * u3, &s1, &c1);
+    int64_t e0 = 2 * q;
+    float2 a = x[e0];
+    y[e0] = make_float2(a.x + sigma * rad0 * c0, a.y + sigma * rad0 * s0);
+    if (e0 + 1 < count) {
+      float2 b = x[e0 + 1];
+      y[e0 + 1] = make_float2(b.x + sigma * rad1 * c1, b.y + sigma * rad1 * s1);
+    }
+  }
+}
+
+// ------------------------------------------------------------ demapper
+// mapping.py:110-143: logits = -|y - p|^2 / no (f64), LLR_j = LSE(bit_j=1) -
+// LSE(bit_j=0) with scipy's max + log1p(sum of the others), or max - max.
+template <int MAXP>
+__global__ void k_demap(const float2 *__restrict__ y, int64_t nsym, double no,
+                        const double *__restrict__ no_vec, const double2 *__restrict__ pts, int m,
+                        int mode, float *__restrict__ llr32, double *__restrict__ llr64) {
+  const int P = 1 << m;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const float2 ys = y[s];
+    const double yr = ys.x, yi = ys.y;
+    const double nos = no_vec ? no_vec[s] : no;
+    double lg[MAXP];
+    for (int p = 0; p < P; ++p) {
+      double dr = yr - pts[p].x, di = yi - pts[p].y;
+      double h = hypot(dr, di);
+      lg[p] = -(h * h) / nos;
+    }
+    for (int j = 0; j < m; ++j) {
+      const int sh = m - 1 - j;
+      double mx1 = -INFINITY, mx0 = -INFINITY;
+      int a1 = -1, a0 = -1;
+      for (int p = 0; p < P; ++p) {
+        if ((p >> sh) & 1) {
+          if (lg[p] > mx1) { mx1 = lg[p]; a1 = p; }
+        } else {
+          if (lg[p] > mx0) { mx0 = lg[p]; a0 = p; }
+        }
+      }
+      double out;
+      if (mode == LS_DEMAP_MAXLOG) {
+        out = mx1 - mx0;
+      } else {
+        double s1 = 0.0, s0 = 0.0;
+        for (int p = 0; p < P; ++p) {
+          if ((p >> sh) & 1) {
+            if (p != a1) s1 += exp(lg[p] - mx1);
+          } else {
+            if (p != a0) s0 += exp(lg[p] - mx0);
+          }
+        }
+        out = (mx1 + log1p(s1)) - (mx0 + log1p(s0));
+      }
+      if (llr32) llr32[s * m + j] = (float)out;
+      if (llr64) llr64[s * m + j] = out;
+    }
+  }
+}
+
+// ------------------------------------------------------------ encoder
+// One CTA per codeword, thread i = circulant lane.  Row syndromes of the
+// systematic part (ldpc.py:308-311, as XORs instead of the GEMM), the
+// accumulate-core solve (ldpc.py:313-320), the extension rows
+// (ldpc.py:327-331), then the rate-matching gather (ldpc.py:351).
+template <class G>
+__global__ void k_encode(QcParams P, const uint8_t *__restrict__ bits, uint8_t *__restrict__ tx,
+                         uint8_t *__restrict__ full) {
+  extern __shared__ uint8_t sm[];
+  const int Z = P.z;
+  uint8_t *cw = sm;                 // [n_full] mother codeword
+  uint8_t *syn = sm + P.n_full;     // [mb * Z]
+  const int64_t b = blockIdx.x;
+  const uint8_t *in = bits + b * (int64_t)P.k;
+  for (int v = threadIdx.x; v < P.k_full; v += blockDim.x) cw[v] = v < P.k ? (in[v] & 1) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
+    for (int r = 0; r < G::MB; ++r) {
+      uint8_t acc = 0;
+      for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
+        const int c = G::d_col(e);
+        if (c < G::KB) {
+          int t = i + P.s[e];
+          t = t >= Z ? t - Z : t;
+          acc ^= cw[c * Z + t];
+        }
+      }
+      syn[r * Z + i] = acc;
+    }
+  }
+  __syncthreads();
+  uint8_t *core = cw + P.k_full;  // p1..p4 blocks
+  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
+    const int im1 = i == 0 ? Z - 1 : i - 1;
+    const uint8_t ss_im1 = syn[im1] ^ syn[Z + im1] ^ syn[2 * Z + im1] ^ syn[3 * Z + im1];
+    const uint8_t ss = syn[i] ^ syn[Z + i] ^ syn[2 * Z + i] ^ syn[3 * Z + i];
+    const uint8_t p1 = ss_im1, p2 = syn[i] ^ ss, p3 = syn[Z + i] ^ p1 ^ p2, p4 = syn[2 * Z + i] ^ p3;
+    core[i] = p1;
+    core[Z + i] = p2;
+    core[2 * Z + i] = p3;
+    core[3 * Z + i] = p4;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
+    for (int r = 4; r < G::MB; ++r) {
+      uint8_t acc = syn[r * Z + i];
+      for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
+        const int c = G::d_col(e);
+        if (c >= G::KB && c < G::KB + 4) {
+          int t = i + P.s[e];
+          t = t >= Z ? t - Z : t;
+          acc ^= core[(c - G::KB) * Z + t];
+        }
+      }
+      cw[P.k_full + r * Z + i] = acc;
+    }
+  }
+  __syncthreads();
+  if (full) {
+    uint8_t *o = full + b * (int64_t)P.n_full;
+    for (int v = threadIdx.x; v < P.n_full; v += blockDim.x) o[v] = cw[v];
+  }
+  if (tx) {
+    uint8_t *o = tx + b * (int64_t)P.n;
+    for (int j = threadIdx.x; j < P.n; j += blockDim.x) o[j] = cw[mother_of(P, j)];
+  }
+}
+
+// ------------------------------------------------------------ derate_match
+// ldpc.py:335-345: mother = +0.0, np.add.at over transmit_idx in index order,
+// fillers = -40.
+template <typename T>
+__global__ void k_derate(QcParams P, const T *__restrict__ llr, int64_t batch, T *__restrict__ mother) {
+  const int64_t total = batch * (int64_t)P.n_full;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / P.n_full;
+    const int v = (int)(t - b * P.n_full);
+    T acc = (T)0;
+    if (v >= P.k && v < P.k_full) {
+      acc = (T)-40.0;
+    } else if (v >= 2 * P.z) {
+      const int pos = v < P.k ? v - 2 * P.z : P.l1 + (v - P.k_full);
+      const T *row = llr + b * P.n;
+      for (int j = pos; j < P.n; j += P.buflen) acc = acc + row[j];
+    }
+    mother[t] = acc;
+  }
+}
+
+// ------------------------------------------------------------ count_errors
+__global__ void k_count(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, int64_t len,
+                        unsigned long long *__restrict__ counts) {
+  const int64_t r = blockIdx.x;
+  unsigned long long e = 0;
+  for (int64_t j = threadIdx.x; j < len; j += blockDim.x) e += (a[r * len + j] != b[r * len + j]);
+  __shared__ unsigned long long red[32];
+  for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    if (t) {
+      atomicAdd(&counts[0], t);
+      atomicAdd(&counts[1], 1ULL);
+    }
+  }
+}
+
+}  // namespace lsb
+
+using namespace lsb;
+
+extern "C" {
+
+const char *ls_last_error(void) { return g_err.c_str(); }
+int ls_version(void) { return 1; }
+
+int ls_code_create(int bg, int z, int k, int n, int mb, int nb, int kb, const int32_t *entries,
+                   int nnz, ls_code **out) {
+  if (!out || !entries) return fail(LS_EINVAL, "ls_code_create: null argument");
+  if (bg != 1 && bg != 2) return fail(LS_EINVAL, "unknown base graph " + std::to_string(bg));
+  if (k < 1 || n <= k)
+    return fail(LS_EINVAL, "unsupported (k=" + std::to_string(k) + ", n=" + std::to_string(n) +
+                               "): need 0 < k < n");
+  if (z < 2 || z > 384) return fail(LS_EINVAL, "lifting size must be in [2, 384]");
+  const int wmb = bg == 1 ? BG1Tables::MB : BG2Tables::MB;
+  const int wnb = bg == 1 ? BG1Tables::NB : BG2Tables::NB;
+  const int wkb = bg == 1 ? BG1Tables::KB : BG2Tables::KB;
+  const int wnnz = bg == 1 ? BG1Tables::NNZ : BG2Tables::NNZ;
+  const int *wrow = bg == 1 ? BG1Tables::row : BG2Tables::row;
+  const int *wcol = bg == 1 ? BG1Tables::col : BG2Tables::col;
+  if (mb != wmb || nb != wnb || kb != wkb || nnz != wnnz)
+    return fail(LS_EINVAL, "base graph dimensions do not match the compiled BG tables");
+  if (k > kb * z) return fail(LS_EINVAL, "k=" + std::to_string(k) + " too large for Z");
+  ls_code *c = new ls_code();
+  QcParams &P = c->p;
+  P.bg = bg; P.z = z; P.k = k; P.n = n; P.mb = mb; P.nb = nb; P.kb = kb; P.nnz = nnz;
+  P.k_full = kb * z;
+  P.n_full = nb * z;
+  P.m_full = mb * z;
+  P.l1 = std::max(0, k - 2 * z);
+  P.buflen = P.l1 + (P.n_full - P.k_full);
+  for (int e = 0; e < nnz; ++e) {
+    const int r = entries[3 * e], col = entries[3 * e + 1], s = entries[3 * e + 2];
+    if (r != wrow[e] || col != wcol[e]) {
+      delete c;
+      return fail(LS_EINVAL, "base graph entries do not match the compiled BG structure");
+    }
+    c->entries[3 * e] = r;
+    c->entries[3 * e + 1] = col;
+    c->entries[3 * e + 2] = s;
+    P.s[e] = (uint16_t)(((s % z) + z) % z);
+  }
+  *out = c;
+  return LS_OK;
+}
+
+int ls_code_destroy(ls_code *code) {
+  delete code;
+  return LS_OK;
+}
+
+int ls_code_transmit_idx(const ls_code *code, int32_t *host_out) {
+  if (!code || !host_out) return fail(LS_EINVAL, "ls_code_transmit_idx: null argument");
+  for (int j = 0; j < code->p.n; ++j) host_out[j] = mother_of(code->p, j);
+  return LS_OK;
+}
+
+int ls_binary_source(uint64_t seed, uint64_t stream_id, int64_t count, uint8_t *bits, void *stream) {
+  if (count < 0 || (!bits && count)) return fail(LS_EINVAL, "binary_source: bad arguments");
+  if (!count) return LS_OK;
+  const int64_t nblk = (count + 31) / 32;
+  k_binary_source<<<grid_for(nblk, 256), 256, 0, as_stream(stream)>>>(seed, stream_id, count, bits);
+  LS_CHECK_LAUNCH("ls_binary_source");
+  return LS_OK;
+}
+
+int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, float *x, void *stream) {
+  if (m < 1 || m > 12) return fail(LS_EINVAL, "num_bits_per_symbol must be in [1, 12]");
+  if (!nsym) return LS_OK;
+  k_map_bits<<<grid_for(nsym, 256), 256, 0, as_stream(stream)>>>(
+      bits, nsym, m, reinterpret_cast<const float2 *>(points), reinterpret_cast<float2 *>(x));
+  LS_CHECK_LAUNCH("ls_map_bits");
+  return LS_OK;
+}
+
+int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id, float *y,
+            void *stream) {
+  if (no < 0) return fail(LS_EINVAL, "noise variance must be >= 0, got " + std::to_string(no));
+  if (!count) return LS_OK;
+  if (no == 0) {
+    cudaError_t e = cudaMemcpyAsync(y, x, (size_t)count * 8, cudaMemcpyDeviceToDevice, as_stream(stream));
+    return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_awgn");
+  }
+  k_awgn<<<grid_for((count + 1) / 2, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float2 *>(x), count, (float)sqrt(no / 2.0), seed, stream_id,
+      reinterpret_cast<float2 *>(y));
+  LS_CHECK_LAUNCH("ls_awgn");
+  return LS_OK;
+}
+
+int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *points64,
+             int m, int mode, float *llr32, double *llr64, void *stream) {
+  if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
+  if (m < 1 || m > 8) return fail(LS_EINVAL, "demap: num_bits_per_symbol must be in [1, 8]");
+  if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
+  if (!nsym) return LS_OK;
+  const float2 *yy = reinterpret_cast<const float2 *>(y);
+  const double2 *pp = reinterpret_cast<const double2 *>(points64);
+  cudaStream_t s = as_stream(stream);
+  if (m <= 4)
+    k_demap<16><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+  else if (m <= 6)
+    k_demap<64><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+  else
+    k_demap<256><<<grid_for(nsym, 64), 64, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+  LS_CHECK_LAUNCH("ls_demap");
+  return LS_OK;
+}
+
+int ls_encode(const ls_code *code, const uint8_t *bits, int64_t batch, uint8_t *tx, uint8_t *full,
+              void *stream) {
+  if (!code) return fail(LS_EINVAL, "ls_encode: null code");
+  if (!batch) return LS_OK;
+  const QcParams &P = code->p;
+  const int threads = std::min(384, ((P.z + 31) / 32) * 32);
+  const size_t smem = (size_t)P.n_full + (size_t)P.mb * P.z;
+  cudaStream_t s = as_stream(stream);
+  if (P.bg == 1) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_encode<BG1Tables>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_encode<BG1Tables><<<(unsigned)batch, threads, smem, s>>>(P, bits, tx, full);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_encode<BG2Tables>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_encode<BG2Tables><<<(unsigned)batch, threads, smem, s>>>(P, bits, tx, full);
+  }
+  LS_CHECK_LAUNCH("ls_encode");
+  return LS_OK;
+}
+
+int ls_derate(const ls_code *code, const void *llr, int is_f64, int64_t batch, void *mother, void *stream) {
+  if (!code) return fail(LS_EINVAL, "ls_derate: null code");
+  if (!batch) return LS_OK;
+  const int64_t total = batch * code->p.n_full;
+  cudaStream_t s = as_stream(stream);
+  if (is_f64)
+    k_derate<double><<<grid_for(total, 256), 256, 0, s>>>(code->p, (const double *)llr, batch, (double *)mother);
+  else
+    k_derate<float><<<grid_for(total, 256), 256, 0, s>>>(code->p, (const float *)llr, batch, (float *)mother);
+  LS_CHECK_LAUNCH("ls_derate");
+  return LS_OK;
+}
+
+int ls_count_errors(const uint8_t *b, const uint8_t *b_hat, int64_t batch, int64_t len,
+                    unsigned long long *counts, void *stream) {
+  if (!batch || !len) return LS_OK;
+  k_count<<<(unsigned)batch, 256, 0, as_stream(stream)>>>(b, b_hat, len, counts);
+  LS_CHECK_LAUNCH("ls_count_errors");
+  return LS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+"""Drop-in mirror of linksim.ldpc (ldpc.py:1-365) on the B200 path.
+
+* `LdpcCode5G(k, n)` selects base graph / lifting size / rate matching
+  exactly as the reference (ldpc.py:214-272) and owns an ls_code handle.
+* `ldpc5g_encode` runs the QC encoder kernel.
+* `bp_decode` runs the EXACT-mode GPU decoder on any ParityCheckMatrix:
+  bit-identical to the reference for min-sum / scaled-min-sum, and the
+  reference's precision pattern for sum-product (LLRs within tolerance).
+* `ldpc5g_decode(..., mode="exact")` (default) is derate_match + exact BP;
+  `mode="fast"` is the on-chip QC decoder fused with rate matching, hard
+  decision and error counting (fp32, statistically equivalent; hard
+  decisions identical on every block that converges).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+from .alist import ParityCheckMatrix
+from .basegraph import base_graph
+from .core import LLR_MAX
+
+BP_VARIANTS = ("sum-product", "min-sum", "scaled-min-sum")
+_VARIANT_ID = {v: i for i, v in enumerate(BP_VARIANTS)}
+
+_LIFT_BASES = (2, 3, 5, 7, 9, 11, 13, 15)
+LIFTING_SIZES = sorted({a * (1 << j) for a in _LIFT_BASES for j in range(8) if a * (1 << j) <= 384})
+
+
+def _base(bg: int):
+    ent, mb, nb, kb = base_graph(bg)
+    return {(int(r), int(c)): int(s) for r, c, s in ent}, mb, nb, kb
+
+
+class _CodeHandle:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and L._lib is not None:
+                L._lib.ls_code_destroy(self.h)
+        except Exception:  # pragma: no cover
+            pass
+
+
+class LdpcCode5G:
+    """5G-style lifted LDPC code with rate matching (ldpc.py:214-345)."""
+
+    def __init__(self, k: int, n: int, *, base_graph: int | None = None, z: int | None = None):
+        self.k, self.n = int(k), int(n)
+        if self.k < 1 or self.n <= self.k:
+            raise ValueError(f"unsupported (k={self.k}, n={self.n}): need 0 < k < n")
+        # BG2 iff k <= 292, smallest Z with k_b*Z >= k (ldpc.py:232-238).  The
+        # keyword overrides lift any graph at any Z for the decoder-only sweep
+        # (BG2 with Z >= 32 is unreachable otherwise).
+        self.base_graph = base_graph if base_graph is not None else (2 if self.k <= 292 else 1)
+        entries, mb, nb, kb = _base(self.base_graph)
+        if self.k > kb * 384:
+            raise ValueError(f"k={self.k} too large for both base graphs")
+        if z is None:
+            z = next((zz for zz in LIFTING_SIZES if kb * zz >= self.k), None)
+            if z is None:
+                raise ValueError(f"no lifting size supports k={self.k}")
+        elif kb * z < self.k:
+            raise ValueError(f"lifting size {z} too small for k={self.k}")
+        self.z = int(z)
+        self._entries = entries
+        self._mb, self._nb, self._kb = mb, nb, kb
+        Z = self.z
+        self.k_full, self.n_full, self.m_full = kb * Z, nb * Z, mb * Z
+        self.num_fillers = self.k_full - self.k
+        self.filler_idx = np.arange(self.k, self.k_full)
+        keep = np.ones(self.n_full, dtype=bool)
+        keep[self.filler_idx] = False
+        keep[: 2 * Z] = False
+        buffer = np.flatnonzero(keep)
+        self.transmit_idx = buffer[np.arange(self.n) % len(buffer)]
+        self._ext_parity = [(r, c - kb, s % Z) for (r, c), s in entries.items()
+                            if kb <= c < kb + 4 and r >= 4]
+        self._pcm = None
+        self._handle = None
+
+    @property
+    def coderate(self) -> float:
+        return self.k / self.n
+
+    # ------------------------------------------------------------ device handle
+    @property
+    def handle(self):
+        if self._handle is None:
+            ent = np.array(sorted((r, c, s) for (r, c), s in self._entries.items()), dtype=np.int32)
+            h = ctypes.c_void_p()
+            L.call("ls_code_create", self.base_graph, self.z, self.k, self.n, self._mb, self._nb,
+                   self._kb, ent.ctypes.data, len(ent), ctypes.byref(h))
+            self._handle = _CodeHandle(h)
+        return self._handle.h
+
+    @property
+    def pcm(self) -> ParityCheckMatrix:
+        """Lifted mother-code matrix: CN r*Z+i <-> VN c*Z+(i+s)%Z (ldpc.py:278-296)."""
+        if self._pcm is None:
+            Z = self.z
+            i = np.arange(Z)
+            rows, cols = [], []
+            for (r, c), s in self._entries.items():
+                rows.append(r * Z + i)
+                cols.append(c * Z + (i + s) % Z)
+            rows = np.concatenate(rows)
+            cols = np.concatenate(cols)
+            order = np.lexsort((cols, rows))
+            rows, cols = rows[order], cols[order]
+            ptr = np.zeros(self.m_full + 1, np.int64)
+            ptr[1:] = np.cumsum(np.bincount(rows, minlength=self.m_full))
+            self._pcm = ParityCheckMatrix._trusted(self.n_full, self.m_full, ptr, cols)
+        return self._pcm
+
+    # ------------------------------------------------------------ encoder
+    def encode_full(self, bits, device: bool = False):
+        """Mother codeword [batch, n_full] (ldpc.py:298-333)."""
+        return _encode(bits, self, full=True, device=device)
+
+    def derate_match(self, llr, device: bool = False):
+        """Rate-matched LLRs -> mother positions (ldpc.py:335-345)."""
+        was_np = not L.is_tensor(llr)
+        t = L.to_device(llr)
+        if t.dim() == 1:
+            t = t.unsqueeze(0)
+        torch = L.torch()
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        if t.shape[-1] != self.n:
+            raise ValueError(f"expected {self.n} LLRs, got {t.shape[-1]}")
+        out = L.empty((t.shape[0], self.n_full), "float64" if t.dtype == torch.float64 else "float32")
+        L.call("ls_derate", self.handle, L.ptr(t), int(t.dtype == torch.float64), t.shape[0],
+               L.ptr(out), L.stream_ptr())
+        return L.to_host(out) if (was_np and not device) else out
+
+
+def _encode(bits, code: LdpcCode5G, full: bool, device: bool):
+    was_np = not L.is_tensor(bits)
+    t = L.to_device(bits, "uint8")
+    if t.dim() == 1:
+        t = t.unsqueeze(0)
+    if t.shape[-1] != code.k:
+        raise ValueError(f"expected {code.k} info bits, got {t.shape[-1]}")
+    B = t.shape[0]
+    out = L.empty((B, code.n_full if full else code.n), "uint8")
+    L.call("ls_encode", code.handle, L.ptr(t), B, None if full else L.ptr(out),
+           L.ptr(out) if full else None, L.stream_ptr())
+    return L.to_host(out) if (was_np and not device) else out
+
+
+def ldpc5g_encode(bits, code: LdpcCode5G, device: bool = False):
+    """[batch, k] info bits -> rate-matched [batch, n] (ldpc.py:348-351)."""
+    return _encode(bits, code, full=False, device=device)
+
+
+def _check_variant(variant: str, num_iter: int):
+    if variant not in BP_VARIANTS:
+        raise ValueError(f"unknown BP variant {variant!r}")
+    if num_iter < 1:
+        raise ValueError("num_iter must be >= 1")
+
+
+def bp_decode(llr, pcm: ParityCheckMatrix, num_iter: int = 20, variant: str = "sum-product",
+              scale: float = 0.75, early_stop: bool = True, *, return_iters: bool = False,
+              device: bool = False):
+    """Flooding BP (ldpc.py:86-172), exact mode, on the GPU.
+
+    Returns (llr_out, hard) [batch, n] like the reference; with
+    return_iters=True also the per-row iteration counts.
+    """
+    _check_variant(variant, num_iter)
+    was_np = not L.is_tensor(llr)
+    torch = L.torch()
+    t = L.to_device(llr)
+    if t.dim() == 1:
+        t = t.unsqueeze(0)
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    if t.shape[-1] != pcm.n:
+        raise ValueError(f"LLR length {t.shape[-1]} does not match n={pcm.n}")
+    B = t.shape[0]
+    is64 = t.dtype == torch.float64
+    out = L.empty((B, pcm.n), "float64" if is64 else "float32")
+    hard = L.empty((B, pcm.n), "uint8")
+    iters = L.empty((B,), "int32")
+    L.call("ls_bp_decode", pcm.device_graph(), L.ptr(t), int(is64), B, int(num_iter), _VARIANT_ID[variant],
+           float(scale), int(bool(early_stop)), L.ptr(out), L.ptr(hard), L.ptr(iters), L.stream_ptr())
+    if was_np and not device:
+        res = (L.to_host(out), L.to_host(hard))
+        return res + (L.to_host(iters),) if return_iters else res
+    return (out, hard, iters) if return_iters else (out, hard)
+
+
+def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum-product",
+                  scale: float = 0.75, *, mode: str = "exact", early_stop: bool = True,
+                  device: bool = False):
+    """BP-decode rate-matched LLRs -> [batch, k] info bits (ldpc.py:354-365)."""
+    _check_variant(variant, num_iter)
+    if mode == "exact":
+        mother = code.derate_match(llr, device=True)
+        _, hard = bp_decode(mother, code.pcm, num_iter, variant, scale, early_stop, device=True)
+        out = hard[:, : code.k].contiguous()
+        return L.to_host(out) if (not L.is_tensor(llr) and not device) else out
+    if mode != "fast":
+        raise ValueError(f"unknown decoder mode {mode!r}")
+    res = qc_decode(llr, code, num_iter, variant, scale, early_stop=early_stop)
+    return L.to_host(res["hard"]) if (not L.is_tensor(llr) and not device) else res["hard"]
+
+
+def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum", scale: float = 0.75,
+              *, early_stop: bool = True, ref_bits=None, want_hard: bool = True, want_llr: bool = False,
+              want_iters: bool = False, counts=None):
+    """Fast-mode fused decoder: rate-matched f32 LLRs [B, n] on the device ->
+    dict(hard [B,k] uint8, llr [B,n_full] f32 mother LLRs, iters [B] int32,
+    counts [2] int64 (bit, block) errors vs ref_bits), each only if asked."""
+    _check_variant(variant, num_iter)
+    t = L.to_device(llr, "float32")
+    if t.dim() == 1:
+        t = t.unsqueeze(0)
+    if t.shape[-1] != code.n:
+        raise ValueError(f"expected {code.n} LLRs, got {t.shape[-1]}")
+    B = t.shape[0]
+    res = {}
+    hard = L.empty((B, code.k), "uint8") if want_hard else None
+    lo = L.empty((B, code.n_full), "float32") if want_llr else None
+    it = L.empty((B,), "int32") if want_iters else None
+    ref = L.to_device(ref_bits, "uint8") if ref_bits is not None else None
+    if ref is not None and counts is None:
+        counts = L.zeros((2,), "int64")
+    L.call("ls_qc_decode", code.handle, L.ptr(t), B, int(num_iter), _VARIANT_ID[variant], float(scale),
+           int(bool(early_stop)), L.ptr(hard), L.ptr(lo), L.ptr(it), L.ptr(ref), L.ptr(counts),
+           L.stream_ptr())
+    res.update(hard=hard, llr=lo, iters=it, counts=counts)
+    return res
+
+
+def exit_mutual_information(llr, bits) -> float:
+    """I = 1 - E[log2(1 + exp(-(2b-1) L))] clipped to [0, 1] (ldpc.py:175-188)."""
+    torch = L.torch()
+    tl = L.to_device(llr, "float64")
+    tb = L.to_device(bits, "float64")
+    if tl.numel() == 0:
+        raise ValueError("exit_mutual_information: empty input")
+    if tuple(tl.shape) != tuple(tb.shape):
+        raise ValueError("exit_mutual_information: shape mismatch")
+    x = torch.clamp(-(2.0 * tb - 1.0) * tl, -LLR_MAX, LLR_MAX)
+    info = 1.0 - torch.mean(torch.log2(1.0 + torch.exp(x)))
+    return float(torch.clamp(info, 0.0, 1.0))

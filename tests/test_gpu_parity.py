@@ -1,0 +1,319 @@
+"""GPU parity tests: the CUDA path (through the C-ABI, via the Python mirror)
+against the oracle and the reference-minted golden vectors.
+
+Bars (north_star / SURVEY.md 8c): bit-exact for bits, codewords, rate
+matching maps, payload RNG and min-sum / scaled-min-sum BP outputs (exact
+mode); demapper LLRs within 1e-9 relative of the f64 reference; sum-product
+exact-mode LLRs within 1e-4 relative with identical hard decisions; fast mode
+identical hard decisions on every converged block and statistically
+equivalent error counts.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2203_11854_b200 as lb  # noqa: E402
+from oracle import linksim_oracle as O  # noqa: E402
+
+
+def unpack(a, count):
+    return np.unpackbits(a, axis=-1, count=count)
+
+
+# ------------------------------------------------------------------ RNG
+def test_binary_source_bit_exact(golden):
+    z = golden("rng")
+    for i in range(3):
+        seed, sid = (int(x) for x in z[f"key{i}"])
+        got = lb.binary_source([3, 100], lb.RngStream(seed, sid))
+        assert got.dtype == np.uint8
+        assert np.array_equal(got, z[f"bits{i}"])
+
+
+@pytest.mark.parametrize("count", [1, 31, 32, 33, 1000, 8448 * 37 + 5])
+def test_binary_source_matches_oracle_sizes(count):
+    got = lb.binary_source([count], lb.RngStream(123, 456))
+    assert np.array_equal(got, O.binary_source((count,), 123, 456))
+
+
+def test_binary_source_errors():
+    with pytest.raises(ValueError):
+        lb.binary_source([0, 3], lb.RngStream(1))
+
+
+# ------------------------------------------------------------------ encoder / rate matching
+@pytest.mark.parametrize("i", range(9))
+def test_encoder_bit_exact(golden, i):
+    e = golden("encoder")
+    k, n, bg, z = (int(x) for x in e[f"k{i}"])
+    code = lb.LdpcCode5G(k, n)
+    assert (code.base_graph, code.z) == (bg, z)
+    bits = unpack(e[f"bits{i}"], k)
+    assert np.array_equal(np.packbits(code.encode_full(bits), axis=-1), e[f"full{i}"])
+    assert np.array_equal(np.packbits(lb.ldpc5g_encode(bits, code), axis=-1), e[f"tx{i}"])
+    assert np.array_equal(code.transmit_idx, e[f"tidx{i}"])
+    import ctypes
+    from paper_2203_11854_b200 import _lib as L
+    tid = np.empty(n, np.int32)
+    L.call("ls_code_transmit_idx", code.handle, tid.ctypes.data)
+    assert np.array_equal(tid, e[f"tidx{i}"])
+    assert np.array_equal(code.derate_match(e[f"derate_in{i}"]), e[f"derate_out{i}"])
+    d64 = e[f"derate_in{i}"].astype(np.float64)
+    assert np.array_equal(code.derate_match(d64), O.Code(k, n).derate_match(d64))
+
+
+def test_encoder_large_batch_parity_and_linearity():
+    code = lb.LdpcCode5G(8448, 16896)
+    oc = O.code(8448, 16896)
+    bits = lb.binary_source([256, 8448], lb.RngStream(5, 9))
+    full = code.encode_full(bits)
+    assert np.array_equal(full[:8], oc.encode_full(bits[:8]))
+    # H c = 0 for every codeword (size-independent property, ldpc.py:278-296)
+    assert not code.pcm.syndrome(full[:32]).any()
+    a, b = bits[:64], bits[64:128]
+    assert np.array_equal(code.encode_full(a ^ b), code.encode_full(a) ^ code.encode_full(b))
+
+
+# ------------------------------------------------------------------ mapping / demapping
+@pytest.mark.parametrize("m", [2, 4, 6])
+def test_map_and_demap(golden, m):
+    d = golden("demap")
+    const = lb.Constellation("qam", m)
+    assert np.array_equal(const.points, d[f"points{m}"])
+    got = lb.map_bits(d[f"mbits{m}"], const)
+    assert np.array_equal(got, d[f"mapped{m}"].astype(np.complex64))
+    for no in (0.05, 0.5):
+        app = lb.demap_app(d[f"y{m}"], no, const)
+        ref = d[f"app{m}_{no}"]
+        assert np.allclose(app, ref, rtol=1e-9, atol=1e-9)
+        ml = lb.demap_maxlog(d[f"y{m}"], no, const)
+        assert np.allclose(ml, d[f"maxlog{m}_{no}"], rtol=1e-9, atol=1e-9)
+
+
+def test_demap_per_symbol_noise_and_errors():
+    const = lb.Constellation("qam", 4)
+    g = np.random.default_rng(3)
+    y = (g.normal(size=(2, 50)) + 1j * g.normal(size=(2, 50))).astype(np.complex64)
+    no = g.uniform(0.1, 1.0, size=(2, 50))
+    got = lb.demap_app(y, no, const)
+    ref = O.demap(y, no, const.points, 4, "app")
+    assert np.allclose(got, ref, rtol=1e-9, atol=1e-9)
+    with pytest.raises(ValueError):
+        lb.demap_app(y, 0.0, const)
+
+
+def test_chain_stage_llrs_match_golden(golden):
+    for cfg in ("c1", "c2", "c4"):
+        d = golden(f"chain_{cfg}")
+        k, n, m, B, _, _ = (int(x) for x in d["dims"])
+        const = lb.Constellation("qam", m)
+        code = lb.LdpcCode5G(k, n)
+        payload = unpack(d["payload"], k)
+        coded = lb.ldpc5g_encode(payload, code)
+        assert np.array_equal(np.packbits(coded, axis=-1), d["coded"])
+        assert np.array_equal(lb.map_bits(coded, const), d["x"])
+        no = float(d["no"])
+        llr = lb.demap_app(d["y"], no, const)
+        assert np.allclose(llr, d["llr_app"], rtol=1e-9, atol=1e-9)
+        llr32 = lb.demap_app(d["y"], no, const, out_dtype="float32")
+        assert np.abs(llr32 - d["llr"]).max() <= 1e-5 * max(1.0, np.abs(d["llr"]).max())
+
+
+# ------------------------------------------------------------------ exact BP
+HAMMING_VARIANTS = ["sum-product", "min-sum", "scaled-min-sum"]
+
+
+@pytest.mark.parametrize("variant", HAMMING_VARIANTS)
+@pytest.mark.parametrize("es", [0, 1])
+@pytest.mark.parametrize("dt", ["64", "32"])
+def test_bp_exact_hamming(golden, variant, es, dt):
+    h = golden("hamming")
+    pcm = lb.ParityCheckMatrix.from_dense(h["H"])
+    lo, hard = lb.bp_decode(h["llr" + dt], pcm, 7, variant, 0.75, bool(es))
+    tag = variant.replace("-", "_")
+    ref = h[f"{tag}_{es}_{dt}_out"]
+    assert lo.dtype == ref.dtype
+    assert np.array_equal(hard, h[f"{tag}_{es}_{dt}_hard"])
+    if variant == "sum-product":
+        assert np.allclose(lo, ref, rtol=1e-4, atol=1e-4)
+    else:
+        assert np.array_equal(lo, ref)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c4"])
+def test_bp_exact_5g_chain(golden, cfg):
+    d = golden(f"chain_{cfg}")
+    k, n, m, B, _, _ = (int(x) for x in d["dims"])
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    for variant in HAMMING_VARIANTS:
+        tag = variant.replace("-", "_")
+        if f"{tag}_llr_out" not in d:
+            continue
+        lo, hard, iters = lb.bp_decode(d["mother"], code.pcm, 20, variant, 0.75, True, return_iters=True)
+        ref = d[f"{tag}_llr_out"]
+        assert np.array_equal(np.packbits(hard, axis=-1), d[f"{tag}_hard"])
+        _, _, it_o = O.bp_decode_csr(d["mother"], *oc._csr, oc.n_full, 20, variant, 0.75, True)
+        assert np.array_equal(iters, it_o)
+        if variant == "sum-product":
+            rel = np.abs(lo - ref) / np.maximum(np.abs(ref), 1.0)
+            assert (rel <= 1e-4).mean() >= 0.999
+            assert np.array_equal(np.sign(lo), np.sign(ref))
+        else:
+            assert np.array_equal(lo, ref)
+        dec = lb.ldpc5g_decode(d["llr"], code, 20, variant)
+        assert np.array_equal(np.packbits(dec, axis=-1), d[f"{tag}_decoded"])
+        if f"{tag}_nes_llr_out" in d:
+            lo2, hard2 = lb.bp_decode(d["mother"], code.pcm, 20, variant, 0.75, False)
+            assert np.array_equal(np.packbits(hard2, axis=-1), d[f"{tag}_nes_hard"])
+            if variant != "sum-product":
+                assert np.array_equal(lo2, d[f"{tag}_nes_llr_out"])
+
+
+def test_bp_exact_matches_oracle_larger_batch():
+    """min-sum exact mode vs the oracle on 96 fresh BG2 codewords in the waterfall."""
+    k, n = 256, 512
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    _, llr = _oracle_llrs(k, n, 2, 1.5, 96, 77)
+    mother = oc.derate_match(llr)
+    for variant in ("min-sum", "scaled-min-sum"):
+        lo, hard, it = lb.bp_decode(mother, code.pcm, 20, variant, 0.75, True, return_iters=True)
+        lo_o, hard_o, it_o = O.bp_decode_csr(mother, *oc._csr, oc.n_full, 20, variant, 0.75, True)
+        assert np.array_equal(lo, lo_o)
+        assert np.array_equal(it, it_o)
+
+
+def test_bp_decode_errors():
+    pcm = lb.ParityCheckMatrix.from_dense(np.array([[1, 1, 0], [0, 1, 1]], np.uint8))
+    with pytest.raises(ValueError):
+        lb.bp_decode(np.zeros((1, 3)), pcm, variant="offset")
+    with pytest.raises(ValueError):
+        lb.bp_decode(np.zeros((1, 3)), pcm, num_iter=0)
+    with pytest.raises(ValueError):
+        lb.bp_decode(np.zeros((1, 4)), pcm)
+
+
+# ------------------------------------------------------------------ fast QC decoder
+def _oracle_llrs(k, n, m, ebno, B, seed):
+    oc = O.code(k, n)
+    bits = O.binary_source((B, k), seed, 1)
+    pts = O.qam_points(m)
+    x = O.map_bits(oc.encode(bits), pts, m).astype(np.complex64)
+    no = O.ebnodb2no(ebno, m, k / n)
+    y = O.awgn_single(x, no, seed, 2)
+    return bits, O.demap(y, no, pts, m).astype(np.float32)
+
+
+@pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 2.0), (8448, 16896, 4, 4.2), (4096, 12288, 6, 0.8),
+                                        (500, 1000, 4, 4.5), (4096, 8192, 2, 1.5)])
+@pytest.mark.parametrize("variant", ["min-sum", "scaled-min-sum"])
+def test_fast_decoder_converged_blocks_identical(k, n, m, ebno, variant):
+    B = 64 if k < 5000 else 16
+    bits, llr = _oracle_llrs(k, n, m, ebno, B, 11)
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    res = lb.qc_decode(llr, code, 20, variant, 0.75, early_stop=True, ref_bits=bits, want_llr=True,
+                       want_iters=True)
+    hard = res["hard"].cpu().numpy()
+    ref_hard, lo_o, it_o = O.decode(llr, oc, 20, variant, 0.75, True)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    ok_fast = (hard == bits).all(axis=1)
+    conv = (it_o < 20) & ok_ref
+    # every block the reference converges on is decoded identically
+    assert np.array_equal(hard[conv], ref_hard[conv])
+    # block-error indicator agrees except on (rare) chaotic failing blocks
+    assert (ok_ref != ok_fast).sum() <= max(1, B // 16)
+    cnt = res["counts"].cpu().numpy()
+    assert cnt[0] == int((hard != bits).sum())
+    assert cnt[1] == int((~ok_fast).sum())
+
+
+def test_fast_decoder_noiseless_round_trip_and_early_stop():
+    for k, n in [(500, 1000), (100, 300), (8448, 16896), (4096, 12288), (256, 1536)]:
+        code = lb.LdpcCode5G(k, n)
+        bits = lb.binary_source([32, k], lb.RngStream(8))
+        tx = lb.ldpc5g_encode(bits, code)
+        llr = ((2.0 * tx - 1.0) * 8.0).astype(np.float32)
+        for es in (True, False):
+            res = lb.qc_decode(llr, code, 30, "min-sum", early_stop=es, want_iters=True)
+            assert np.array_equal(res["hard"].cpu().numpy(), bits)
+            it = res["iters"].cpu().numpy()
+            assert (it == (1 if es else 30)).all()
+
+
+def test_fast_decoder_fixed_iterations_llr_close_to_exact_on_clean_rows():
+    k, n = 4096, 8192
+    bits, llr = _oracle_llrs(k, n, 2, 3.0, 16, 5)
+    code = lb.LdpcCode5G(k, n)
+    res = lb.qc_decode(llr, code, 20, "min-sum", early_stop=False, want_llr=True)
+    lo_fast = res["llr"].cpu().numpy()
+    lo_ex, _ = lb.bp_decode(code.derate_match(llr), code.pcm, 20, "min-sum", early_stop=False)
+    # saturated (|L| = 40) decisions agree in sign everywhere on converged rows
+    assert np.array_equal(np.sign(lo_fast[:, :k]), np.sign(lo_ex[:, :k]))
+
+
+# ------------------------------------------------------------------ channel / counting / pipeline
+def test_awgn_statistics_and_determinism():
+    x = np.zeros((64, 4096), np.complex64)
+    y1 = lb.awgn(x, 0.5, lb.RngStream(1, 2))
+    y2 = lb.awgn(x, 0.5, lb.RngStream(1, 2))
+    y3 = lb.awgn(x, 0.5, lb.RngStream(1, 3))
+    assert np.array_equal(y1, y2)
+    assert not np.array_equal(y1, y3)
+    assert abs(y1.real.mean()) < 0.01 and abs(y1.imag.mean()) < 0.01
+    assert abs(np.mean(np.abs(y1) ** 2) - 0.5) < 0.01
+    assert abs(y1.real.var() - 0.25) < 0.01
+    assert np.array_equal(lb.awgn(x + 1, 0.0, lb.RngStream(1)), x + 1)
+    with pytest.raises(ValueError):
+        lb.awgn(x, -1.0, lb.RngStream(1))
+
+
+def test_count_errors_and_metrics():
+    g = np.random.default_rng(0)
+    a = g.integers(0, 2, (50, 300), dtype=np.uint8)
+    b = a.copy()
+    b[3, 7] ^= 1
+    b[9, :5] ^= 1
+    assert lb.count_errors(a, b) == O.count_errors(a, b) == (6, 2)
+    assert lb.compute_ber(a, b) == pytest.approx(6 / a.size)
+    assert lb.compute_bler(a, b) == pytest.approx(2 / 50)
+    with pytest.raises(ValueError):
+        lb.count_errors(a, b[:, :3])
+
+
+def test_pipeline_run_batch_payload_matches_reference_stream(golden):
+    d = golden("chain_c1")
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": 256, "n": 512, "decoder": {"variant": "min-sum"}},
+        "modulation": {"kind": "qam", "bits_per_symbol": 2},
+        "sweep": {"ebno_db": [2.0], "batch_size": 48}, "seed": 42})
+    pipe = lb.Pipeline(cfg)
+    payload, dec = pipe.run_batch(2.0, 48, lb.RngStream(42, (1 << 32) | 1))
+    assert np.array_equal(np.packbits(payload, axis=-1), d["payload"])
+    assert dec.shape == payload.shape
+
+
+def test_run_sweep_statistics_close_to_oracle():
+    """BER/BLER of the GPU sweep inside the oracle's 95% Monte-Carlo interval."""
+    k, n, m, ebno, B = 256, 512, 2, 2.5, 512
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"variant": "min-sum", "mode": "fast"}},
+        "modulation": {"kind": "qam", "bits_per_symbol": m},
+        "sweep": {"ebno_db": [ebno], "batch_size": B, "target_block_errors": 10**9,
+                  "max_batches_per_point": 8}, "seed": 42})
+    res = lb.run_sweep(cfg)
+    p = res.points[0]
+    assert p.blocks == 8 * B
+    errs = 0
+    for b in range(2):
+        pl, dec = O.run_batch(k, n, m, ebno, B, 42, (1 << 32) | (b + 1), "min-sum")
+        errs += int((pl != dec).any(axis=1).sum())
+    bler_ref = errs / (2 * B)
+    sd = np.sqrt(bler_ref * (1 - bler_ref) / (2 * B) + p.bler * (1 - p.bler) / p.blocks)
+    assert abs(p.bler - bler_ref) <= 2.6 * sd + 1e-3
