@@ -156,7 +156,7 @@ class Clocks:
         sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
         mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[j] for s in self.samples for j in range(4) if "Active" in s[3 + j]})
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if s[3 + j] == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.samples)}
 

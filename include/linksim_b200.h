@@ -120,11 +120,18 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
  * (core.py:93-99): one CTA per codeword, messages on chip.  llr [B,n] f32
  * rate-matched.  Outputs (all nullable): hard_k [B,k] info bits,
  * llr_out [B,n_full] f32 mother LLRs (ln p1/p0), iters_used [B],
- * counts[2] += (bit errors, block errors) against ref_bits [B,k]. */
+ * counts[2] += (bit errors, block errors) against ref_bits [B,k].
+ * flags: LS_QC_PRUNE skips the dead extension rows whose parity bit is never
+ * transmitted (their llr_out entries are then the channel values);
+ * LS_QC_GENERIC forces the runtime-Z kernel instead of a specialised one. */
+#define LS_QC_PRUNE 1
+#define LS_QC_GENERIC 2
 int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
-                 double scale, int early_stop, uint8_t *hard_k, float *llr_out,
+                 double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,
                  int32_t *iters_used, const uint8_t *ref_bits, unsigned long long *counts,
                  void *stream);
+/* Number of base rows the fast decoder processes with LS_QC_PRUNE. */
+int ls_qc_live_rows(const ls_code *code);
 
 /* count_errors(b, b_hat) (core.py:93-99): counts[2] += (bit, block) errors. */
 int ls_count_errors(const uint8_t *b, const uint8_t *b_hat, int64_t batch, int64_t len,

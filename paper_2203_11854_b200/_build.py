@@ -23,15 +23,41 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
          "-I", os.path.join(ROOT, "include")]
 
 
-def _deps():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    files.append(os.path.join(ROOT, "include", "linksim_b200.h"))
-    return files
+GEN = os.path.join(ROOT, "build", "gen")
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _instance_sources():
+    """One translation unit per specialised fast-decoder instance listed in
+    csrc/qc_instances.h, so they compile in parallel."""
+    import re
+
+    text = open(os.path.join(CSRC, "qc_instances.h")).read()
+    os.makedirs(GEN, exist_ok=True)
+    out = []
+    for bg, z, r in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+)\)", text):
+        name = f"qc_{bg}_{z}_{r}.cu"
+        body = (f'#include "{CSRC}/bp_fast_qc.cuh"\n'
+                "namespace lsb {\n"
+                f"int qc2_{bg}_{z}_{r}(const QcChanParams &P, const float *l, int64_t B, int it, float a, int es,\n"
+                "    uint8_t *h, float *lo, int32_t *iu, const uint8_t *ref, unsigned long long *cnt, cudaStream_t s) {\n"
+                f"  return launch_qc_fast2<BG{bg}Tables, {z}, {r}>(P, l, B, it, a, es, h, lo, iu, ref, cnt, s);\n"
+                "}\n}  // namespace lsb\n")
+        path = os.path.join(GEN, name)
+        if not os.path.exists(path) or open(path).read() != body:
+            with open(path, "w") as f:
+                f.write(body)
+        out.append(path)
+    return out
+
+
+
+
+def _compile(src: str, verbose: bool, newest_hdr: float, force: bool) -> str:
+    obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
+    if (not force and os.path.exists(obj)
+            and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_hdr)):
+        return obj
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -47,12 +73,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     from tools import gen_bg_header
 
     gen_bg_header.main()
-    newest = max(os.path.getmtime(f) for f in _deps())
+    srcs = [os.path.join(CSRC, f) for f in SOURCES] + _instance_sources()
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hdrs.append(os.path.join(ROOT, "include", "linksim_b200.h"))
+    newest_hdr = max(os.path.getmtime(f) for f in hdrs)
+    newest = max(newest_hdr, max(os.path.getmtime(f) for f in srcs))
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    with concurrent.futures.ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    with concurrent.futures.ThreadPoolExecutor(min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose, newest_hdr, force), srcs))
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

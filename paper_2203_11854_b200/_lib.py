@@ -40,7 +40,8 @@ _SIGS = {
     "ls_encode": [_vp, _vp, _i64, _vp, _vp, _vp],
     "ls_derate": [_vp, _vp, _int, _i64, _vp, _vp],
     "ls_bp_decode": [_vp, _vp, _int, _i64, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp],
-    "ls_qc_decode": [_vp, _vp, _i64, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ls_qc_decode": [_vp, _vp, _i64, _int, _int, _dbl, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ls_qc_live_rows": [_vp],
     "ls_count_errors": [_vp, _vp, _i64, _i64, _vp, _vp],
 }
 

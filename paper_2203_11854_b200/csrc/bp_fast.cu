@@ -24,7 +24,9 @@
 #include <algorithm>
 #include <type_traits>
 
+#include "bp_fast_qc.cuh"
 #include "common.cuh"
+#include "qc_instances.h"
 
 namespace lsb {
 
@@ -206,15 +208,48 @@ static int launch_fast(const QcFastParams &FP, const float *llr, int64_t B, int 
 
 using namespace lsb;
 
+namespace lsb {
+#define LSB_QC_DECL(bg, z, r)                                                                                   \
+  int qc2_##bg##_##z##_##r(const QcChanParams &, const float *, int64_t, int, float, int, uint8_t *, float *, \
+                           int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
+LSB_QC_INSTANCES(LSB_QC_DECL)
+#define LSB_QC_ENTRY(bg, z, r) {bg, z, r, &qc2_##bg##_##z##_##r},
+static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
+
+// rows whose degree-1 extension column holds at least one transmitted bit:
+// the transmitted mother positions are a prefix of the circular buffer
+// (ldpc.py:252-256), so the live rows are a prefix 0..R-1
+int live_rows(const QcParams &P) {
+  if (P.n >= P.buflen) return P.mb;
+  const int last = mother_of(P, P.n - 1);
+  const int r = last / P.z - P.kb + 1;
+  return r < 4 ? 4 : (r > P.mb ? P.mb : r);
+}
+}  // namespace lsb
+
+extern "C" int ls_qc_live_rows(const ls_code *code) { return code ? live_rows(code->p) : -1; }
+
 extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
-                            double scale, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,
-                            const uint8_t *ref_bits, unsigned long long *counts, void *stream) {
+                            double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,
+                            int32_t *iters_used, const uint8_t *ref_bits, unsigned long long *counts,
+                            void *stream) {
   if (!code) return fail(LS_EINVAL, "ls_qc_decode: null code");
   if (variant < 0 || variant > 2) return fail(LS_EINVAL, "unknown BP variant");
   if (num_iter < 1) return fail(LS_EINVAL, "num_iter must be >= 1");
   if (variant == LS_SUM_PRODUCT) return fail(LS_EINVAL, "ls_qc_decode: sum-product fast mode not built yet");
   if (batch <= 0) return LS_OK;
   const QcParams &P = code->p;
+  const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
+  cudaStream_t s = as_stream(stream);
+  if (!(flags & LS_QC_GENERIC)) {
+    const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
+    for (const QcKernelEntry &k : kQcKernels) {
+      if (k.bg == P.bg && k.z == P.z && k.r == R) {
+        QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
+        return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
+      }
+    }
+  }
   QcFastParams FP;
   FP.z = P.z; FP.k = P.k; FP.n = P.n; FP.k_full = P.k_full; FP.n_full = P.n_full; FP.l1 = P.l1;
   FP.buflen = P.buflen;
@@ -224,8 +259,6 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
     FP.lo[e] = 4 * (c * P.z + s);
     FP.hi[e] = 4 * (c * P.z + s - P.z);
   }
-  const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
-  cudaStream_t s = as_stream(stream);
   if (P.bg == 1)
     return launch_fast<BG1Tables, LS_MIN_SUM>(FP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out,
                                               iters_used, ref_bits, counts, s);

@@ -212,12 +212,21 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
     return L.to_host(res["hard"]) if (not L.is_tensor(llr) and not device) else res["hard"]
 
 
+LS_QC_PRUNE, LS_QC_GENERIC = 1, 2
+
+
 def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum", scale: float = 0.75,
               *, early_stop: bool = True, ref_bits=None, want_hard: bool = True, want_llr: bool = False,
-              want_iters: bool = False, counts=None):
+              want_iters: bool = False, counts=None, prune: bool | None = None, generic: bool = False):
     """Fast-mode fused decoder: rate-matched f32 LLRs [B, n] on the device ->
     dict(hard [B,k] uint8, llr [B,n_full] f32 mother LLRs, iters [B] int32,
-    counts [2] int64 (bit, block) errors vs ref_bits), each only if asked."""
+    counts [2] int64 (bit, block) errors vs ref_bits), each only if asked.
+
+    prune (default: on unless mother LLRs are requested) skips the dead
+    extension rows whose parity bit is never transmitted."""
+    if prune is None:
+        prune = not want_llr
+    flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
     _check_variant(variant, num_iter)
     t = L.to_device(llr, "float32")
     if t.dim() == 1:
@@ -233,7 +242,7 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
     if ref is not None and counts is None:
         counts = L.zeros((2,), "int64")
     L.call("ls_qc_decode", code.handle, L.ptr(t), B, int(num_iter), _VARIANT_ID[variant], float(scale),
-           int(bool(early_stop)), L.ptr(hard), L.ptr(lo), L.ptr(it), L.ptr(ref), L.ptr(counts),
+           int(bool(early_stop)), flags, L.ptr(hard), L.ptr(lo), L.ptr(it), L.ptr(ref), L.ptr(counts),
            L.stream_ptr())
     res.update(hard=hard, llr=lo, iters=it, counts=counts)
     return res
