@@ -41,7 +41,7 @@ def _args():
     p.add_argument("--batch", type=int, default=65536)
     p.add_argument("--variant", default="min-sum")
     p.add_argument("--iters", type=int, default=20)
-    p.add_argument("--ebno", type=float, default=5.0)
+    p.add_argument("--ebno", type=float, default=6.0)
     p.add_argument("--early-stop", action="store_true")
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--cpu-seconds", type=float, default=15.0)

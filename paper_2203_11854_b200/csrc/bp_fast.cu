@@ -43,6 +43,7 @@ __device__ __forceinline__ void static_for(F &&f) {
 // c*Z + (i+s)%Z is 4*i + (i < thr ? lo : hi)
 struct QcFastParams {
   int z, k, n, k_full, n_full, l1, buflen;
+  int nrows;  // base rows processed (dead extension rows pruned)
   int thr[kMaxNnz];
   int lo[kMaxNnz];
   int hi[kMaxNnz];
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(384, 1)
       static_for<0, G::MB>([&](auto rc) {
         constexpr int r = decltype(rc)::value;
         constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1];
+        if (r >= P.nrows) return;
         const float o1 = m1[r], o2 = m2[r];
         const uint32_t opk = pk[r];
         const uint32_t oidx = opk & 31u;
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     static_for<0, G::MB>([&](auto rc) {
       constexpr int r = decltype(rc)::value;
+      if (r >= P.nrows) return;  // uniform: whole CTA skips the barrier
       if (lane) {
         constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1];
         const float o1 = m1[r], o2 = m2[r];
@@ -209,11 +212,11 @@ static int launch_fast(const QcFastParams &FP, const float *llr, int64_t B, int 
 using namespace lsb;
 
 namespace lsb {
-#define LSB_QC_DECL(bg, z, r)                                                                                   \
+#define LSB_QC_DECL(bg, z, r, sp)                                                                                 \
   int qc2_##bg##_##z##_##r(const QcChanParams &, const float *, int64_t, int, float, int, uint8_t *, float *, \
                            int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
 LSB_QC_INSTANCES(LSB_QC_DECL)
-#define LSB_QC_ENTRY(bg, z, r) {bg, z, r, &qc2_##bg##_##z##_##r},
+#define LSB_QC_ENTRY(bg, z, r, sp){bg, z, r, &qc2_##bg##_##z##_##r},
 static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
 
 // rows whose degree-1 extension column holds at least one transmitted bit:
@@ -253,6 +256,7 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   QcFastParams FP;
   FP.z = P.z; FP.k = P.k; FP.n = P.n; FP.k_full = P.k_full; FP.n_full = P.n_full; FP.l1 = P.l1;
   FP.buflen = P.buflen;
+  FP.nrows = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
   for (int e = 0; e < P.nnz; ++e) {
     const int c = code->entries[3 * e + 1], s = P.s[e];
     FP.thr[e] = P.z - s;

@@ -210,8 +210,11 @@ def _oracle_llrs(k, n, m, ebno, B, seed):
     return bits, O.demap(y, no, pts, m).astype(np.float32)
 
 
-@pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 2.0), (8448, 16896, 4, 4.2), (4096, 12288, 6, 0.8),
-                                        (500, 1000, 4, 4.5), (4096, 8192, 2, 1.5)])
+# Eb/N0 points where the reference's min-sum converges on most (not all)
+# blocks, located with the oracle (64-QAM r=1/3 on the synthetic graph needs
+# ~7 dB)
+@pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 3.5), (8448, 16896, 4, 5.8), (4096, 12288, 6, 7.0),
+                                        (500, 1000, 4, 6.0), (4096, 8192, 2, 3.0)])
 @pytest.mark.parametrize("variant", ["min-sum", "scaled-min-sum"])
 def test_fast_decoder_converged_blocks_identical(k, n, m, ebno, variant):
     B = 64 if k < 5000 else 16
@@ -225,6 +228,7 @@ def test_fast_decoder_converged_blocks_identical(k, n, m, ebno, variant):
     ok_ref = (ref_hard == bits).all(axis=1)
     ok_fast = (hard == bits).all(axis=1)
     conv = (it_o < 20) & ok_ref
+    assert conv.sum() >= B // 4, "test point must exercise converged blocks"
     # every block the reference converges on is decoded identically
     assert np.array_equal(hard[conv], ref_hard[conv])
     # block-error indicator agrees except on (rare) chaotic failing blocks
@@ -242,21 +246,26 @@ def test_fast_decoder_noiseless_round_trip_and_early_stop():
         llr = ((2.0 * tx - 1.0) * 8.0).astype(np.float32)
         # rows with untransmitted (dead) parity checks need a second
         # iteration: their signed-zero messages leave the syndrome unsatisfied
-        # after the first one, exactly as in the reference
+        # after the first one, exactly as in the reference; with the dead
+        # rows pruned every clean block stops after one iteration
         _, _, it_ref = O.decode(llr, O.code(k, n), 30, "min-sum", 0.75, True)
         for es in (True, False):
-            res = lb.qc_decode(llr, code, 30, "min-sum", early_stop=es, want_iters=True)
-            assert np.array_equal(res["hard"].cpu().numpy(), bits)
-            it = res["iters"].cpu().numpy()
-            assert np.array_equal(it, it_ref if es else np.full(32, 30))
+            for prune in (False, True):
+                res = lb.qc_decode(llr, code, 30, "min-sum", early_stop=es, want_iters=True, prune=prune)
+                assert np.array_equal(res["hard"].cpu().numpy(), bits)
+                it = res["iters"].cpu().numpy()
+                if not es:
+                    assert (it == 30).all()
+                elif prune:  # a partially transmitted last row keeps some dead checks
+                    assert (it <= it_ref).all() and (it >= 1).all()
+                else:
+                    assert np.array_equal(it, it_ref)
 
 
-@pytest.mark.parametrize("k,n,m,ebno", [(8448, 16896, 4, 4.3), (4096, 8192, 2, 1.6), (4096, 12288, 6, 0.8),
-                                        (256, 512, 2, 2.0)])
+@pytest.mark.parametrize("k,n,m,ebno", [(8448, 16896, 4, 5.8), (4096, 8192, 2, 3.0), (4096, 12288, 6, 7.0),
+                                        (256, 512, 2, 3.5)])
 def test_specialised_decoder_equals_generic_kernel(k, n, m, ebno):
-    """The compile-time (BG, Z, R) kernels are the runtime-Z kernel with
-    immediates: bit-identical outputs with all rows; with dead rows pruned
-    the block-error indicator and converged blocks are unchanged."""
+    """The compile-time (BG, Z, R) kernels against the runtime-Z kernel."""
     B = 24 if k > 5000 else 64
     bits, llr = _oracle_llrs(k, n, m, ebno, B, 3)
     code = lb.LdpcCode5G(k, n)
@@ -264,13 +273,22 @@ def test_specialised_decoder_equals_generic_kernel(k, n, m, ebno):
         a = lb.qc_decode(llr, code, 20, "min-sum", early_stop=es, want_llr=True, want_iters=True, prune=False)
         g = lb.qc_decode(llr, code, 20, "min-sum", early_stop=es, want_llr=True, want_iters=True, prune=False,
                          generic=True)
-        for key in ("hard", "llr", "iters"):
-            assert torch.equal(a[key], g[key]), key
         p = lb.qc_decode(llr, code, 20, "min-sum", early_stop=es, want_iters=True, prune=True)
-        ha, hp = a["hard"].cpu().numpy(), p["hard"].cpu().numpy()
-        ok_a, ok_p = (ha == bits).all(1), (hp == bits).all(1)
-        assert np.array_equal(hp[ok_a & ok_p], ha[ok_a & ok_p])
-        assert (ok_a != ok_p).sum() <= max(1, B // 16)
+        hg = g["hard"].cpu().numpy()
+        ok_g = (hg == bits).all(1)
+        assert ok_g.sum() >= B // 4
+        for other in (a, p):
+            # the specialised kernels may sum the rows in a different order
+            # (threads per lane > 1) and may prune dead rows: converged
+            # blocks and the block-error indicator must not change
+            ho = other["hard"].cpu().numpy()
+            ok_o = (ho == bits).all(1)
+            both = ok_g & ok_o
+            assert np.array_equal(ho[both], hg[both])
+            assert (ok_g != ok_o).sum() <= max(1, B // 16)
+            if es:
+                it_g, it_o = g["iters"].cpu().numpy(), other["iters"].cpu().numpy()
+                assert np.abs(it_g[both] - it_o[both]).max(initial=0) <= 1
 
 
 def test_fast_decoder_fixed_iterations_llr_close_to_exact_on_clean_rows():
@@ -279,9 +297,13 @@ def test_fast_decoder_fixed_iterations_llr_close_to_exact_on_clean_rows():
     code = lb.LdpcCode5G(k, n)
     res = lb.qc_decode(llr, code, 20, "min-sum", early_stop=False, want_llr=True)
     lo_fast = res["llr"].cpu().numpy()
-    lo_ex, _ = lb.bp_decode(code.derate_match(llr), code.pcm, 20, "min-sum", early_stop=False)
-    # saturated (|L| = 40) decisions agree in sign everywhere on converged rows
-    assert np.array_equal(np.sign(lo_fast[:, :k]), np.sign(lo_ex[:, :k]))
+    lo_ex, hard_ex = lb.bp_decode(code.derate_match(llr), code.pcm, 20, "min-sum", early_stop=False)
+    ok_ex = (hard_ex[:, :k] == bits).all(1)
+    ok_fast = (lo_fast[:, :k] > 0).astype(np.uint8)
+    ok_fast = (ok_fast == bits).all(1)
+    assert ok_ex.mean() >= 0.9 and np.array_equal(ok_ex, ok_fast)
+    # on every converged row the mother-code LLR signs agree everywhere
+    assert np.array_equal(np.sign(lo_fast[ok_ex]), np.sign(lo_ex[ok_ex]))
 
 
 # ------------------------------------------------------------------ channel / counting / pipeline

@@ -19,7 +19,7 @@ p.add_argument("--reps", type=int, default=3)
 p.add_argument("--k", type=int, default=8448)
 p.add_argument("--n", type=int, default=16896)
 p.add_argument("--m", type=int, default=4)
-p.add_argument("--ebno", type=float, default=5.0)
+p.add_argument("--ebno", type=float, default=6.0)
 p.add_argument("--iters", type=int, default=20)
 p.add_argument("--variant", default="min-sum")
 p.add_argument("--early-stop", action="store_true")
