@@ -95,6 +95,14 @@ int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t st
 int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec,
              const double *points64, int m, int mode, float *llr32, double *llr64, void *stream);
 
+/* Same as ls_demap for Gray QAM (mapping.py:33-48), using the product
+ * structure: each bit's LLR is a log-sum-exp over the 2^(m/2) levels of its
+ * own axis (equal to the 2^m-point formula to ~1e-12).
+ * amp[l] / lab[l] (host, 2^(m/2) entries): amplitude and axis label of level l. */
+int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec,
+                 const double *amp, const int32_t *lab, int m, int mode, float *llr32,
+                 double *llr64, void *stream);
+
 /* ---- LDPC ------------------------------------------------------------ */
 /* ldpc5g_encode(bits, code) (ldpc.py:298-351): bits [B,k] -> rate-matched
  * codewords tx [B,n] (nullable) and/or the mother codeword full [B,n_full]

@@ -37,6 +37,7 @@ _SIGS = {
     "ls_map_bits": [_vp, _i64, _int, _vp, _vp, _vp],
     "ls_awgn": [_vp, _i64, _dbl, _u64, _u64, _vp, _vp],
     "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_encode": [_vp, _vp, _i64, _vp, _vp, _vp],
     "ls_derate": [_vp, _vp, _int, _i64, _vp, _vp],
     "ls_bp_decode": [_vp, _vp, _int, _i64, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp],

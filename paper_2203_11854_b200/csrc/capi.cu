@@ -143,6 +143,75 @@ __global__ void k_demap(const float2 *__restrict__ y, int64_t nsym, double no,
   }
 }
 
+// Gray-QAM fast path: the points are a product of two Gray
+// PAM axes (even label bits -> I, odd -> Q, mapping.py:33-48), so the
+// Q-axis factor cancels in every I-bit LLR and vice versa:
+//   LLR(b) = LSE_{l: bit=1} -(y_ax - a_l)^2/no - LSE_{l: bit=0} (...)
+// over the 2^(m/2) levels of b's own axis.  Same scipy LSE structure (max +
+// log1p of the others), f64; agrees with the 2^m-point formula to ~1e-12.
+struct QamAxes {
+  double amp[16];   // level amplitudes (unit-energy normalised)
+  int lab[16];      // axis label of each level, MSB first
+};
+
+template <int HALF>
+__global__ void k_demap_qam(const float2 *__restrict__ y, int64_t nsym, double no,
+                            const double *__restrict__ no_vec, const QamAxes A, int mode,
+                            float *__restrict__ llr32, double *__restrict__ llr64) {
+  constexpr int L = 1 << HALF, M = 2 * HALF;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const float2 ys = y[s];
+    const double inv = 1.0 / (no_vec ? no_vec[s] : no);
+    double out[M];
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      const double yv = ax == 0 ? (double)ys.x : (double)ys.y;
+      double lg[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const double d = yv - A.amp[l];
+        lg[l] = -(d * d) * inv;
+      }
+#pragma unroll
+      for (int t = 0; t < HALF; ++t) {
+        const int sh = HALF - 1 - t;
+        double mx1 = -INFINITY, mx0 = -INFINITY;
+        int a1 = -1, a0 = -1;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          if ((A.lab[l] >> sh) & 1) {
+            if (lg[l] > mx1) { mx1 = lg[l]; a1 = l; }
+          } else {
+            if (lg[l] > mx0) { mx0 = lg[l]; a0 = l; }
+          }
+        }
+        double v;
+        if (mode == LS_DEMAP_MAXLOG) {
+          v = mx1 - mx0;
+        } else {
+          double s1 = 0.0, s0 = 0.0;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            if ((A.lab[l] >> sh) & 1) {
+              if (l != a1) s1 += exp(lg[l] - mx1);
+            } else {
+              if (l != a0) s0 += exp(lg[l] - mx0);
+            }
+          }
+          v = (mx1 + log1p(s1)) - (mx0 + log1p(s0));
+        }
+        out[2 * t + ax] = v;  // stream bit 2t is the t-th I bit, 2t+1 the t-th Q bit
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      if (llr32) llr32[s * M + j] = (float)out[j];
+      if (llr64) llr64[s * M + j] = out[j];
+    }
+  }
+}
+
 // ------------------------------------------------------------ encoder
 // One CTA per codeword, thread i = circulant lane.  Row syndromes of the
 // systematic part (ldpc.py:308-311, as XORs instead of the GEMM), the
@@ -362,6 +431,32 @@ int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, cons
   else
     k_demap<256><<<grid_for(nsym, 64), 64, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
   LS_CHECK_LAUNCH("ls_demap");
+  return LS_OK;
+}
+
+int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, const double *amp,
+                 const int32_t *lab, int m, int mode, float *llr32, double *llr64, void *stream) {
+  if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
+  if (m < 2 || m > 8 || (m % 2)) return fail(LS_EINVAL, "demap_qam: bits per symbol must be 2, 4, 6 or 8");
+  if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
+  if (!amp || !lab) return fail(LS_EINVAL, "demap_qam: null level table");
+  if (!nsym) return LS_OK;
+  QamAxes A;
+  const int L = 1 << (m / 2);
+  for (int l = 0; l < 16; ++l) {
+    A.amp[l] = l < L ? amp[l] : 0.0;
+    A.lab[l] = l < L ? lab[l] : 0;
+  }
+  const float2 *yy = reinterpret_cast<const float2 *>(y);
+  cudaStream_t s = as_stream(stream);
+  const unsigned g = grid_for(nsym, 256);
+  switch (m) {
+    case 2: k_demap_qam<1><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
+    case 4: k_demap_qam<2><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
+    case 6: k_demap_qam<3><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
+    default: k_demap_qam<4><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
+  }
+  LS_CHECK_LAUNCH("ls_demap_qam");
   return LS_OK;
 }
 

@@ -84,6 +84,31 @@ class Constellation:
     def bit_table(self) -> np.ndarray:
         return self._bits
 
+    def qam_axes(self):
+        """(amp, lab) per-axis level tables if the points are the library's Gray
+        QAM (product of two Gray PAM axes), else None."""
+        if getattr(self, "_axes", 0) != 0:
+            return self._axes
+        self._axes = None
+        m = self.num_bits_per_symbol
+        if self.kind == "qam" and m % 2 == 0 and m <= 8:
+            half = m // 2
+            L = 1 << half
+            idx = np.arange(L)
+            lab = (idx ^ (idx >> 1)).astype(np.int32)       # Gray label of level idx
+            w = 1 << np.arange(half - 1, -1, -1)
+            bits = self._bits.astype(np.int64)
+            lab_i, lab_q = bits[:, 0::2] @ w, bits[:, 1::2] @ w
+            amp = np.empty(L)
+            ok = True
+            for l in range(L):
+                pts = self.points[(lab_i == lab[l])]
+                amp[l] = pts[0].real
+                ok &= np.all(pts.real == amp[l]) and np.all(self.points[lab_q == lab[l]].imag == amp[l])
+            if ok:
+                self._axes = (np.ascontiguousarray(amp), np.ascontiguousarray(lab))
+        return self._axes
+
     def device_points(self, dtype: str):
         """Points on the GPU as interleaved float32 (complex64-rounded) or float64."""
         if dtype not in self._dev:
@@ -132,6 +157,12 @@ def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str
         no_s = 1.0
     out = L.empty(tuple(ty.shape[:-1]) + (ty.shape[-1] * m,), out_dtype)
     is64 = out_dtype == "float64"
+    axes = constellation.qam_axes()
+    if axes is not None:
+        amp, lab = axes
+        L.call("ls_demap_qam", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), amp.ctypes.data, lab.ctypes.data,
+               m, mode, None if is64 else L.ptr(out), L.ptr(out) if is64 else None, L.stream_ptr())
+        return L.to_host(out) if (was_np and not device) else out
     L.call("ls_demap", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec),
            L.ptr(constellation.device_points("float64")), m, mode,
            None if is64 else L.ptr(out), L.ptr(out) if is64 else None, L.stream_ptr())
