@@ -34,13 +34,14 @@ def _instance_sources():
     text = open(os.path.join(CSRC, "qc_instances.h")).read()
     os.makedirs(GEN, exist_ok=True)
     out = []
-    for bg, z, r, sp in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", text):
-        name = f"qc_{bg}_{z}_{r}.cu"
-        body = (f'#include "{CSRC}/bp_fast_qc.cuh"\n'
+    for bg, z, r, sp, pr in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\w+)\)", text):
+        name = f"qc_{pr}_{bg}_{z}_{r}.cu"
+        launcher = "launch_qc_fast2" if pr == "f32" else "launch_qc_fast_h2"
+        body = (f'#include "{CSRC}/bp_fast_h2.cuh"\n'
                 "namespace lsb {\n"
-                f"int qc2_{bg}_{z}_{r}(const QcChanParams &P, const float *l, int64_t B, int it, float a, int es,\n"
+                f"int qc2_{pr}_{bg}_{z}_{r}(const QcChanParams &P, const float *l, int64_t B, int it, float a, int es,\n"
                 "    uint8_t *h, float *lo, int32_t *iu, const uint8_t *ref, unsigned long long *cnt, cudaStream_t s) {\n"
-                f"  return launch_qc_fast2<BG{bg}Tables, {z}, {r}, {sp}>(P, l, B, it, a, es, h, lo, iu, ref, cnt, s);\n"
+                f"  return {launcher}<BG{bg}Tables, {z}, {r}, {sp}>(P, l, B, it, a, es, h, lo, iu, ref, cnt, s);\n"
                 "}\n}  // namespace lsb\n")
         path = os.path.join(GEN, name)
         if not os.path.exists(path) or open(path).read() != body:

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <type_traits>
 
+#include "bp_fast_h2.cuh"
 #include "bp_fast_qc.cuh"
 #include "common.cuh"
 #include "qc_instances.h"
@@ -212,11 +213,13 @@ static int launch_fast(const QcFastParams &FP, const float *llr, int64_t B, int 
 using namespace lsb;
 
 namespace lsb {
-#define LSB_QC_DECL(bg, z, r, sp)                                                                                 \
-  int qc2_##bg##_##z##_##r(const QcChanParams &, const float *, int64_t, int, float, int, uint8_t *, float *, \
-                           int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
+#define LSB_QC_DECL(bg, z, r, sp, pr)                                                                   \
+  int qc2_##pr##_##bg##_##z##_##r(const QcChanParams &, const float *, int64_t, int, float, int, uint8_t *, \
+                                  float *, int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
 LSB_QC_INSTANCES(LSB_QC_DECL)
-#define LSB_QC_ENTRY(bg, z, r, sp){bg, z, r, &qc2_##bg##_##z##_##r},
+#define LSB_QC_PREC_f32 0
+#define LSB_QC_PREC_h2 1
+#define LSB_QC_ENTRY(bg, z, r, sp, pr) {bg, z, r, LSB_QC_PREC_##pr, &qc2_##pr##_##bg##_##z##_##r},
 static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
 
 // rows whose degree-1 extension column holds at least one transmitted bit:
@@ -244,14 +247,18 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   const QcParams &P = code->p;
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
+  if ((flags & LS_QC_FP16) && (flags & LS_QC_GENERIC))
+    return fail(LS_EINVAL, "ls_qc_decode: the fp16x2 decoder has no runtime-Z kernel");
   if (!(flags & LS_QC_GENERIC)) {
     const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
+    const int prec = (flags & LS_QC_FP16) ? 1 : 0;
     for (const QcKernelEntry &k : kQcKernels) {
-      if (k.bg == P.bg && k.z == P.z && k.r == R) {
+      if (k.bg == P.bg && k.z == P.z && k.r == R && k.prec == prec) {
         QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
         return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
       }
     }
+    if (prec) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
   }
   QcFastParams FP;
   FP.z = P.z; FP.k = P.k; FP.n = P.n; FP.k_full = P.k_full; FP.n_full = P.n_full; FP.l1 = P.l1;

@@ -1,0 +1,307 @@
+// FAST-mode QC decoder, packed fp16x2 variant (F4): every 32-bit lane word
+// carries the same message of TWO codewords (A in the low half, B in the
+// high half), so one instruction advances both.  Structure, schedule and
+// compile-time specialisation are those of k_qc_fast2 (bp_fast_qc.cuh);
+// the differences are the packed state and arithmetic:
+//   posterior   half2 {A, B} per VN in shared memory
+//   CN state    M1, M2 = half2 {min_A, min_B} (alpha-scaled), IX = half2
+//               {argmin_A, argmin_B} (small integers are exact in fp16), sign
+//               bits in one word for d <= 16 (A: bits 0..15, B: 16..31) or two
+//   per edge    mag   = select(M1, M2, IX == {p,p})        (HSET2 + LOP3)
+//               cold  = mag | signs moved to bits 15/31     (SHF + LOP3)
+//               x     = t - cold                            (HADD2)
+//               min1/min2/argmin update                     (HMNMX2, HSET2, LOP3)
+// Precision: fp16 (11-bit significand) messages and posteriors, as in
+// production 5G decoders; statistically equivalent to the reference and
+// checked like the fp32 kernel (tests/test_gpu_parity.py).
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "bp_fast_qc.cuh"
+
+namespace lsb {
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2 *>(&u); }
+
+__host__ __device__ constexpr int ilog2c(int p) { return p > 1 ? 1 + ilog2c(p >> 1) : 0; }
+
+// half2 {p, p} bit pattern of a small non-negative integer, at compile time
+template <int P>
+__device__ __forceinline__ constexpr uint32_t h2_int() {
+  static_assert(P >= 0 && P < 2048, "integer not exact in fp16");
+  if constexpr (P == 0) {
+    return 0u;
+  } else {
+    constexpr int e = ilog2c(P);
+    constexpr uint32_t h = ((uint32_t)(e + 15) << 10) | (((uint32_t)P - (1u << e)) << (10 - e));
+    return h | (h << 16);
+  }
+}
+
+template <class G, int Z, int R, int SPLIT>
+struct QcShapeH2 {
+  static constexpr int NT1 = ((Z + 31) / 32) * 32;
+  static constexpr int NT = NT1 * SPLIT;
+  static constexpr int NCOL = G::KB + (R > 4 ? R : 4);
+  static constexpr int NV = NCOL * Z;
+  static constexpr int NR = (R + SPLIT - 1) / SPLIT;
+  static constexpr size_t ARR = 4 * (size_t)NV;  // one half2 per VN
+  static constexpr bool CHN_SMEM = (SPLIT + 1) * ARR <= 225 * 1024;
+  static constexpr size_t SMEM = (SPLIT + (CHN_SMEM ? 1 : 0)) * ARR;
+  static constexpr int MINB = NT >= 384 ? 1 : (384 / NT);
+};
+
+// per-codeword outputs of half `HB` (0 = A, 1 = B) from the current posteriors
+template <int NT, int HB>
+__device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *tot, int nv, int64_t cw,
+                                        const float *row, int used, uint8_t *hard_k, float *llr_out,
+                                        int32_t *iters_used, const uint8_t *ref, unsigned long long *counts,
+                                        unsigned *red) {
+  const int t = threadIdx.x;
+  if (iters_used && t == 0) iters_used[cw] = used;
+  if (llr_out) {
+    float *o = llr_out + cw * (int64_t)P.n_full;
+    for (int v = t; v < P.n_full; v += NT) {
+      float val;
+      if (v < nv) {
+        const uint32_t w = tot[v];
+        val = -__half2float(__ushort_as_half((unsigned short)(HB ? (w >> 16) : (w & 0xFFFFu))));
+      } else {
+        val = -chan_value(P, row, v);
+      }
+      o[v] = val;
+    }
+  }
+  unsigned err = 0;
+  for (int v = t; v < P.k; v += NT) {
+    const uint32_t w = tot[v];
+    const unsigned short hb = (unsigned short)(HB ? (w >> 16) : (w & 0xFFFFu));
+    const uint8_t hd = (-__half2float(__ushort_as_half(hb))) > 0.0f;
+    if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
+    if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
+  }
+  if (ref && counts) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+    if ((t & 31) == 0) red[t >> 5] = err;
+    __syncthreads();
+    if (t == 0) {
+      unsigned long long tt = 0;
+      for (int w = 0; w < NT / 32; ++w) tt += red[w];
+      if (tt) {
+        atomicAdd(&counts[0], tt);
+        atomicAdd(&counts[1], 1ULL);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <class G, int Z, int R, int SPLIT>
+__global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z, R, SPLIT>::MINB)
+    k_qc_fast_h2(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
+                 int early_stop, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
+                 int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
+                 unsigned long long *__restrict__ counts) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  extern __shared__ uint32_t smw[];
+  uint32_t *tot = smw;
+  uint32_t *chn = smw + SPLIT * S::NV;
+  __shared__ unsigned red[S::NT / 32];
+  const int t = threadIdx.x;
+  const int h = t / S::NT1;
+  const int i = t - h * S::NT1;
+  const bool lane = i < Z;
+  char *const base = reinterpret_cast<char *>(smw);
+  const int64_t cwA = 2 * (int64_t)blockIdx.x, cwB = cwA + 1;
+  const bool hasB = cwB < batch;
+  const float *rowA = llr + cwA * (int64_t)P.n;
+  const float *rowB = hasB ? rowA + P.n : rowA;
+  const __half2 al2 = __float2half2_rn(alpha);
+  const bool scaled = alpha != 1.0f;
+
+  for (int v = t; v < S::NV; v += S::NT) {
+    const float a = chan_value(P, rowA, v);
+    const float bb = hasB ? chan_value(P, rowB, v) : 40.0f;
+    const uint32_t w = h2u(__floats2half2_rn(a, bb));
+    if constexpr (S::CHN_SMEM) chn[v] = w;
+    tot[v] = w;
+  }
+  uint32_t M1[S::NR], M2[S::NR], IX[S::NR], SG[S::NR], SG2[S::NR];
+#pragma unroll
+  for (int j = 0; j < S::NR; ++j) {
+    M1[j] = 0u;
+    M2[j] = 0u;
+    IX[j] = 0u;
+    SG[j] = 0u;
+    SG2[j] = 0u;
+  }
+  __syncthreads();
+
+  int doneA = 0, doneB = hasB ? 0 : 1;
+  for (int it = 0; it < num_iter; ++it) {
+    // ------------------------------------------------ check-node phase
+    uint32_t synx = 0;
+    if (lane) {
+      sfor<0, SPLIT>([&](auto hc) {
+        constexpr int H = decltype(hc)::value;
+        if (h != H) return;
+        const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
+        sfor<0, S::NR>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          constexpr int r = j * SPLIT + H;
+          if constexpr (r < R) {
+            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
+            constexpr bool packed = d <= 16;
+            const uint32_t o1 = M1[j], o2 = M2[j], oix = IX[j], osg = SG[j], osg2 = SG2[j];
+            uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, nix = 0u, sg = 0u, sg2 = 0u, hs = 0u;
+            sfor<e0, e1>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              constexpr int p = e - e0;
+              const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + vn_off<G, Z, e>(i4));
+              hs ^= tw;
+              const __half2 pp = u2h(h2_int<p>());
+              const uint32_t sel = __heq2_mask(u2h(oix), pp);
+              const uint32_t mag = (o1 & ~sel) | (o2 & sel);
+              uint32_t sgn;
+              if constexpr (packed) {
+                sgn = (osg << (15 - p)) & 0x80008000u;
+              } else {
+                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+              }
+              const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
+              const uint32_t xw = h2u(x);
+              const __half2 a = __habs2(x);
+              const uint32_t lt = __hlt2_mask(a, u2h(n1));
+              nix = (nix & ~lt) | (h2u(pp) & lt);
+              n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
+              n1 = h2u(__hmin2(u2h(n1), a));
+              if constexpr (packed) {
+                sg |= (xw >> (15 - p)) & (0x10001u << p);
+              } else {
+                sg |= ((xw >> 15) & 1u) << p;
+                sg2 |= (xw >> 31) << p;
+              }
+            });
+            constexpr uint32_t dm = (1u << d) - 1u;
+            uint32_t flip;
+            if constexpr (packed) {
+              const uint32_t pa = __popc(sg & 0xFFFFu) & 1u, pb = __popc(sg >> 16) & 1u;
+              flip = ((0u - pa) & dm) | ((0u - pb) & (dm << 16));
+              SG[j] = sg ^ flip;
+            } else {
+              const uint32_t pa = __popc(sg) & 1u, pb = __popc(sg2) & 1u;
+              SG[j] = sg ^ ((0u - pa) & dm);
+              SG2[j] = sg2 ^ ((0u - pb) & dm);
+            }
+            if (scaled) {
+              n1 = h2u(__hmul2(u2h(n1), al2));
+              n2 = h2u(__hmul2(u2h(n2), al2));
+            }
+            M1[j] = n1;
+            M2[j] = n2;
+            IX[j] = nix;
+            synx |= hs;
+          }
+        });
+      });
+    }
+    if (early_stop && it > 0) {
+      // per-codeword syndrome of the posterior left by iteration `it`
+      const int badA = __syncthreads_or(lane && ((synx >> 15) & 1u));
+      const int badB = __syncthreads_or(lane && (synx >> 31));
+      if (!doneA && !badA) {
+        h2_emit<S::NT, 0>(P, tot, S::NV, cwA, rowA, it, hard_k, llr_out, iters_used, ref, counts, red);
+        doneA = 1;
+      }
+      if (!doneB && !badB) {
+        h2_emit<S::NT, 1>(P, tot, S::NV, cwB, rowB, it, hard_k, llr_out, iters_used, ref, counts, red);
+        doneB = 1;
+      }
+      if (doneA && doneB) return;
+    } else {
+      __syncthreads();
+    }
+    // ------------------------------------------------ variable-node phase
+    for (int v = t; v < S::NV; v += S::NT) {
+      uint32_t ch;
+      if constexpr (S::CHN_SMEM) {
+        ch = chn[v];
+      } else {
+        ch = h2u(__floats2half2_rn(chan_value(P, rowA, v), hasB ? chan_value(P, rowB, v) : 40.0f));
+      }
+      tot[v] = ch;
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) tot[q * S::NV + v] = 0u;
+    }
+    __syncthreads();
+    sfor<0, S::NR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      if (lane) {
+        sfor<0, SPLIT>([&](auto hc) {
+          constexpr int H = decltype(hc)::value;
+          constexpr int r = j * SPLIT + H;
+          if constexpr (r < R) {
+            if (h != H) return;
+            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
+            constexpr bool packed = d <= 16;
+            const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
+            char *const arr = base + 4u * H * S::NV;
+            const uint32_t o1 = M1[j], o2 = M2[j], oix = IX[j], osg = SG[j], osg2 = SG2[j];
+            sfor<e0, e1>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              constexpr int p = e - e0;
+              uint32_t *tp = reinterpret_cast<uint32_t *>(arr + vn_off<G, Z, e>(i4));
+              const uint32_t sel = __heq2_mask(u2h(oix), u2h(h2_int<p>()));
+              const uint32_t mag = (o1 & ~sel) | (o2 & sel);
+              uint32_t sgn;
+              if constexpr (packed) {
+                sgn = (osg << (15 - p)) & 0x80008000u;
+              } else {
+                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+              }
+              *tp = h2u(__hadd2(u2h(*tp), u2h(mag | sgn)));
+            });
+          }
+        });
+      }
+      __syncthreads();
+    });
+    const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
+    for (int v = t; v < S::NV; v += S::NT) {
+      __half2 acc = u2h(tot[v]);
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * S::NV + v]));
+      tot[v] = h2u(__hmin2(__hmax2(acc, lo), hi));
+    }
+    __syncthreads();
+  }
+  if (!doneA) h2_emit<S::NT, 0>(P, tot, S::NV, cwA, rowA, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+  if (!doneB) h2_emit<S::NT, 1>(P, tot, S::NV, cwB, rowB, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+}
+
+template <class G, int Z, int R, int SPLIT>
+int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
+                      uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
+                      unsigned long long *counts, cudaStream_t s) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  auto kern = k_qc_fast_h2<G, Z, R, SPLIT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  const int64_t chunk = 2LL * 0x3fffffff;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t nb = B - b0 < chunk ? B - b0 : chunk;
+    kern<<<(unsigned)((nb + 1) / 2), S::NT, S::SMEM, s>>>(
+        P, llr + b0 * P.n, nb, num_iter, alpha, early_stop, hard_k ? hard_k + b0 * P.k : nullptr,
+        llr_out ? llr_out + b0 * P.n_full : nullptr, iters_used ? iters_used + b0 : nullptr,
+        ref ? ref + b0 * P.k : nullptr, counts);
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+}
+
+}  // namespace lsb

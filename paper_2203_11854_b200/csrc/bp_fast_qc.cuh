@@ -266,7 +266,7 @@ int launch_qc_fast2(const QcChanParams &P, const float *llr, int64_t B, int num_
 
 // registry entry: (bg, Z, R) -> launcher, defined by the instantiation units
 struct QcKernelEntry {
-  int bg, z, r;
+  int bg, z, r, prec;  // prec: 0 fp32, 1 fp16x2
   QcLauncher fn;
 };
 

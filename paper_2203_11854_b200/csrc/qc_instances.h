@@ -1,16 +1,23 @@
-// (base graph, Z, processed rows, threads per lane) combinations of the
-// specialised fast decoder that are compiled in.  Each becomes
-// build/gen/qc_<bg>_<z>_<r>.cu.  Codes matching none of them use the
-// runtime-Z kernel in bp_fast.cu.
+// Specialised fast-decoder instances compiled in: (base graph, Z, processed
+// rows, threads per lane, precision).  Each becomes build/gen/qc_<...>.cu.
+// Codes matching none of them use the runtime-Z fp32 kernel in bp_fast.cu.
 //   1,384,24 / 1,384,46 : config 2 (k=8448 n=16896), dead rows pruned / all
 //   1,192,{24,45,46}    : configs 3 and 4 (k=4096, n=8192 / 12288)
 //   2,26,{12,42}        : config 1 (k=256 n=512)
+// precision f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh)
 #pragma once
 #define LSB_QC_INSTANCES(X) \
-  X(1, 384, 24, 2)          \
-  X(1, 384, 46, 2)          \
-  X(1, 192, 24, 4)          \
-  X(1, 192, 45, 2)          \
-  X(1, 192, 46, 2)          \
-  X(2, 26, 12, 1)           \
-  X(2, 26, 42, 1)
+  X(1, 384, 24, 2, f32)     \
+  X(1, 384, 46, 2, f32)     \
+  X(1, 192, 24, 4, f32)     \
+  X(1, 192, 45, 2, f32)     \
+  X(1, 192, 46, 2, f32)     \
+  X(2, 26, 12, 1, f32)      \
+  X(2, 26, 42, 1, f32)      \
+  X(1, 384, 24, 2, h2)      \
+  X(1, 384, 46, 2, h2)      \
+  X(1, 192, 24, 4, h2)      \
+  X(1, 192, 45, 2, h2)      \
+  X(1, 192, 46, 2, h2)      \
+  X(2, 26, 12, 1, h2)       \
+  X(2, 26, 42, 1, h2)

@@ -212,21 +212,26 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
     return L.to_host(res["hard"]) if (not L.is_tensor(llr) and not device) else res["hard"]
 
 
-LS_QC_PRUNE, LS_QC_GENERIC = 1, 2
+LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16 = 1, 2, 4
 
 
 def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum", scale: float = 0.75,
               *, early_stop: bool = True, ref_bits=None, want_hard: bool = True, want_llr: bool = False,
-              want_iters: bool = False, counts=None, prune: bool | None = None, generic: bool = False):
+              want_iters: bool = False, counts=None, prune: bool | None = None, generic: bool = False,
+              precision: str = "fp32"):
     """Fast-mode fused decoder: rate-matched f32 LLRs [B, n] on the device ->
     dict(hard [B,k] uint8, llr [B,n_full] f32 mother LLRs, iters [B] int32,
     counts [2] int64 (bit, block) errors vs ref_bits), each only if asked.
 
     prune (default: on unless mother LLRs are requested) skips the dead
-    extension rows whose parity bit is never transmitted."""
+    extension rows whose parity bit is never transmitted.  precision
+    "fp16x2" selects the packed two-codewords-per-lane kernel."""
     if prune is None:
         prune = not want_llr
-    flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
+    if precision not in ("fp32", "fp16x2"):
+        raise ValueError(f"unknown decoder precision {precision!r}")
+    flags = ((LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
+             | (LS_QC_FP16 if precision == "fp16x2" else 0))
     _check_variant(variant, num_iter)
     t = L.to_device(llr, "float32")
     if t.dim() == 1:

@@ -238,6 +238,41 @@ def test_fast_decoder_converged_blocks_identical(k, n, m, ebno, variant):
     assert cnt[1] == int((~ok_fast).sum())
 
 
+@pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 3.5), (8448, 16896, 4, 5.8), (4096, 12288, 6, 7.0),
+                                        (4096, 8192, 2, 3.0)])
+@pytest.mark.parametrize("variant", ["min-sum", "scaled-min-sum"])
+@pytest.mark.parametrize("es", [True, False])
+def test_fast_fp16x2_decoder(k, n, m, ebno, variant, es):
+    """Packed two-codewords-per-lane kernel: odd batch, converged blocks
+    identical to the reference, block errors statistically equal."""
+    B = 63 if k < 5000 else 15
+    bits, llr = _oracle_llrs(k, n, m, ebno, B, 11)
+    code = lb.LdpcCode5G(k, n)
+    res = lb.qc_decode(llr, code, 20, variant, 0.75, early_stop=es, ref_bits=bits, want_iters=True,
+                       precision="fp16x2")
+    hard = res["hard"].cpu().numpy()
+    ref_hard, _, it_o = O.decode(llr, O.code(k, n), 20, variant, 0.75, True)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    ok_fast = (hard == bits).all(axis=1)
+    conv = (it_o < 20) & ok_ref
+    assert conv.sum() >= B // 4
+    assert np.array_equal(hard[conv], ref_hard[conv])
+    assert (ok_ref != ok_fast).sum() <= max(1, B // 12)
+    cnt = res["counts"].cpu().numpy()
+    assert cnt[0] == int((hard != bits).sum()) and cnt[1] == int((~ok_fast).sum())
+    it = res["iters"].cpu().numpy()
+    if es:
+        assert (it >= 1).all() and (it <= 20).all() and (it[ok_fast] < 20).mean() >= 0.9
+    else:
+        assert (it == 20).all()
+    # clean input: every codeword (incl. the unpaired last one) decodes, 1-2 iterations
+    tx = lb.ldpc5g_encode(bits, code)
+    clean = lb.qc_decode(((2.0 * tx - 1.0) * 8.0).astype(np.float32), code, 20, variant, 0.75,
+                         early_stop=True, want_iters=True, precision="fp16x2")
+    assert np.array_equal(clean["hard"].cpu().numpy(), bits)
+    assert (clean["iters"].cpu().numpy() <= 2).all()
+
+
 def test_fast_decoder_noiseless_round_trip_and_early_stop():
     for k, n in [(500, 1000), (100, 300), (8448, 16896), (4096, 12288), (256, 1536)]:
         code = lb.LdpcCode5G(k, n)

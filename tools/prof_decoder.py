@@ -23,6 +23,7 @@ p.add_argument("--ebno", type=float, default=6.0)
 p.add_argument("--iters", type=int, default=20)
 p.add_argument("--variant", default="min-sum")
 p.add_argument("--early-stop", action="store_true")
+p.add_argument("--precision", default="fp32")
 a = p.parse_args()
 cfg = lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": a.k, "n": a.n},
                               "modulation": {"kind": "qam", "bits_per_symbol": a.m},
@@ -35,7 +36,7 @@ for r in range(a.reps):
     if r == a.reps - 1:
         ev[0].record()
     lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, early_stop=a.early_stop, ref_bits=payload,
-                 want_hard=False, counts=counts)
+                 want_hard=False, counts=counts, precision=a.precision)
 ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1])
