@@ -155,16 +155,20 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
           if constexpr (r < R) {
             constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
             constexpr bool packed = d <= 16;
-            const uint32_t o1 = M1[j], o2 = M2[j], oix = IX[j], osg = SG[j], osg2 = SG2[j];
-            uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, nix = 0u, sg = 0u, sg2 = 0u, hs = 0u;
+            // ALU-pipe relief: the min1/min2 select and the argmin update
+            // are fp16 FMAs on 1.0/0.0 compare results (FMA pipe), and the
+            // sign-bit shift is an IMAD.HI
+            const __half2 o1 = u2h(M1[j]), od = u2h(M2[j]), oix = u2h(IX[j]);
+            const uint32_t osg = SG[j], osg2 = SG2[j];
+            uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u;
+            __half2 nix = u2h(0u);
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
               const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + vn_off<G, Z, e>(i4));
               hs ^= tw;
               const __half2 pp = u2h(h2_int<p>());
-              const uint32_t sel = __heq2_mask(u2h(oix), pp);
-              const uint32_t mag = (o1 & ~sel) | (o2 & sel);
+              const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
               uint32_t sgn;
               if constexpr (packed) {
                 sgn = (osg << (15 - p)) & 0x80008000u;
@@ -175,12 +179,14 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
               const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
               const uint32_t xw = h2u(x);
               const __half2 a = __habs2(x);
-              const uint32_t lt = __hlt2_mask(a, u2h(n1));
-              nix = (nix & ~lt) | (h2u(pp) & lt);
+              nix = __hfma2(__hlt2(a, u2h(n1)), __hsub2(pp, nix), nix);
               n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
               n1 = h2u(__hmin2(u2h(n1), a));
               if constexpr (packed) {
-                sg |= (xw >> (15 - p)) & (0x10001u << p);
+                if constexpr (p == 15)
+                  sg |= xw & 0x80008000u;
+                else
+                  sg |= __umulhi(xw, 1u << (17 + p)) & (0x10001u << p);  // xw >> (15 - p)
               } else {
                 sg |= ((xw >> 15) & 1u) << p;
                 sg2 |= (xw >> 31) << p;
@@ -201,9 +207,11 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
               n1 = h2u(__hmul2(u2h(n1), al2));
               n2 = h2u(__hmul2(u2h(n2), al2));
             }
+            // state keeps min1 and the fp16 difference min2 - min1; the
+            // argmin edge is reconstructed as min1 + diff (within 1 ulp of min2)
             M1[j] = n1;
-            M2[j] = n2;
-            IX[j] = nix;
+            M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
+            IX[j] = h2u(nix);
             synx |= hs;
           }
         });
@@ -250,13 +258,13 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
             constexpr bool packed = d <= 16;
             const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
             char *const arr = base + 4u * H * S::NV;
-            const uint32_t o1 = M1[j], o2 = M2[j], oix = IX[j], osg = SG[j], osg2 = SG2[j];
+            const __half2 o1 = u2h(M1[j]), od = u2h(M2[j]), oix = u2h(IX[j]);
+            const uint32_t osg = SG[j], osg2 = SG2[j];
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
               uint32_t *tp = reinterpret_cast<uint32_t *>(arr + vn_off<G, Z, e>(i4));
-              const uint32_t sel = __heq2_mask(u2h(oix), u2h(h2_int<p>()));
-              const uint32_t mag = (o1 & ~sel) | (o2 & sel);
+              const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
               uint32_t sgn;
               if constexpr (packed) {
                 sgn = (osg << (15 - p)) & 0x80008000u;
