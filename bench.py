@@ -196,7 +196,7 @@ def run_b200(a, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=a.early_stop, ref_bits=payload,
-                     want_hard=False, counts=counts)
+                     want_hard=False, counts=counts, precision=pipe.precision)
         if timed:
             e1.record(stream)
             dec_events.append((e0, e1))
@@ -240,12 +240,13 @@ def run_b200(a, rank, world, local_rank):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random payload per step)",
-            "config": _workload(a),
-            "gpu_launches": 6 * a.steps,
+            "vs_baseline": None, "dtype": "f16x2" if pipe.precision == "fp16x2" else "f32",
+            "data": "synthetic (random payload per step)",
+            "config": dict(_workload(a), decoder_precision=pipe.precision, fused_modem=pipe.fused_modem),
+            "gpu_launches": (4 if pipe.fused_modem else 6) * a.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_qc_fast (fused derate+BP+hard+count)",
+                         "kernel": "k_qc_fast_h2" if pipe.precision == "fp16x2" else "k_qc_fast2",
                          "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
                          "kernel_ms_per_launch": per_launch_ms,
                          "kernel_share_of_step": dec_ms / ms,

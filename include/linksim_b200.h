@@ -103,6 +103,15 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec,
                  const double *amp, const int32_t *lab, int m, int mode, float *llr32,
                  double *llr64, void *stream);
 
+/* Fused map_bits -> awgn -> demap_app|maxlog for Gray QAM (sweep.py:352-356
+ * in one pass): coded bits [nsym*m] -> f32 LLRs [nsym*m].  The noisy symbols
+ * equal ls_map_bits + ls_awgn with the same (seed, stream_id); the per-axis
+ * log-sum-exp runs in f32.  points: 2^m complex64 (device); amp/lab as in
+ * ls_demap_qam (host; lab[l] must be the Gray label l ^ (l >> 1)). */
+int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, const double *amp,
+                 const int32_t *lab, double no, uint64_t seed, uint64_t stream_id, int mode,
+                 float *llr, void *stream);
+
 /* ---- LDPC ------------------------------------------------------------ */
 /* ldpc5g_encode(bits, code) (ldpc.py:298-351): bits [B,k] -> rate-matched
  * codewords tx [B,n] (nullable) and/or the mother codeword full [B,n_full]
@@ -141,6 +150,9 @@ int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_i
                  void *stream);
 /* Number of base rows the fast decoder processes with LS_QC_PRUNE. */
 int ls_qc_live_rows(const ls_code *code);
+/* 1 if a compile-time specialised kernel serves this code with these flags
+ * (LS_QC_PRUNE / LS_QC_FP16), else 0 (fp32 falls back to the runtime-Z kernel). */
+int ls_qc_has_kernel(const ls_code *code, int flags);
 
 /* count_errors(b, b_hat) (core.py:93-99): counts[2] += (bit, block) errors. */
 int ls_count_errors(const uint8_t *b, const uint8_t *b_hat, int64_t batch, int64_t len,

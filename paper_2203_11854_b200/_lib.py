@@ -38,11 +38,13 @@ _SIGS = {
     "ls_awgn": [_vp, _i64, _dbl, _u64, _u64, _vp, _vp],
     "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "ls_modem_qam": [_vp, _i64, _int, _vp, _vp, _vp, _dbl, _u64, _u64, _int, _vp, _vp],
     "ls_encode": [_vp, _vp, _i64, _vp, _vp, _vp],
     "ls_derate": [_vp, _vp, _int, _i64, _vp, _vp],
     "ls_bp_decode": [_vp, _vp, _int, _i64, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp],
     "ls_qc_decode": [_vp, _vp, _i64, _int, _int, _dbl, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp],
     "ls_qc_live_rows": [_vp],
+    "ls_qc_has_kernel": [_vp, _int],
     "ls_count_errors": [_vp, _vp, _i64, _i64, _vp, _vp],
 }
 

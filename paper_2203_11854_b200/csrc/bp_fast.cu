@@ -235,6 +235,15 @@ int live_rows(const QcParams &P) {
 
 extern "C" int ls_qc_live_rows(const ls_code *code) { return code ? live_rows(code->p) : -1; }
 
+extern "C" int ls_qc_has_kernel(const ls_code *code, int flags) {
+  if (!code) return 0;
+  const int R = (flags & LS_QC_PRUNE) ? live_rows(code->p) : code->p.mb;
+  const int prec = (flags & LS_QC_FP16) ? 1 : 0;
+  for (const QcKernelEntry &k : kQcKernels)
+    if (k.bg == code->p.bg && k.z == code->p.z && k.r == R && k.prec == prec) return 1;
+  return 0;
+}
+
 extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
                             double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,
                             int32_t *iters_used, const uint8_t *ref_bits, unsigned long long *counts,

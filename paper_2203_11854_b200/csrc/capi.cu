@@ -69,26 +69,110 @@ __global__ void k_map_bits(const uint8_t *__restrict__ bits, int64_t nsym, int m
 // ------------------------------------------------------------ awgn (fast mode)
 // Counter-based: element pair q uses Philox4x32 counter (q, stream lo, stream hi, 0)
 // under key (seed lo, seed hi); Box-Muller gives two complex normals per call.
+// standard complex normals (unit variance per real component) for complex
+// elements 2q and 2q+1 of stream (seed, sid)
+__device__ __forceinline__ void normal_pair(int64_t q, uint64_t seed, uint64_t sid, float2 &n0, float2 &n1) {
+  uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)sid, (uint32_t)(sid >> 32)),
+                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  // uniforms in (0,1] and [0,1)
+  float u0 = ((r.x >> 8) + 1) * (1.0f / 16777216.0f), u1 = (r.y >> 8) * (1.0f / 16777216.0f);
+  float u2 = ((r.z >> 8) + 1) * (1.0f / 16777216.0f), u3 = (r.w >> 8) * (1.0f / 16777216.0f);
+  float rad0 = sqrtf(-2.0f * logf(u0)), rad1 = sqrtf(-2.0f * logf(u2));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  n0 = make_float2(rad0 * c0, rad0 * s0);
+  n1 = make_float2(rad1 * c1, rad1 * s1);
+}
+
 __global__ void k_awgn(const float2 *__restrict__ x, int64_t count, float sigma, uint64_t seed,
                        uint64_t sid, float2 *__restrict__ y) {
   const int64_t npair = (count + 1) / 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
        q += (int64_t)gridDim.x * blockDim.x) {
-    uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)sid, (uint32_t)(sid >> 32)),
-                            make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-    // uniforms in (0,1] and [0,1)
-    float u0 = ((r.x >> 8) + 1) * (1.0f / 16777216.0f), u1 = (r.y >> 8) * (1.0f / 16777216.0f);
-    float u2 = ((r.z >> 8) + 1) * (1.0f / 16777216.0f), u3 = (r.w >> 8) * (1.0f / 16777216.0f);
-    float rad0 = sqrtf(-2.0f * logf(u0)), rad1 = sqrtf(-2.0f * logf(u2));
-    float s0, c0, s1, c1;
-    sincospif(2.0f * u1, &s0, &c0);
-    sincospif(2.0f * u3, &s1, &c1);
+    float2 n0, n1;
+    normal_pair(q, seed, sid, n0, n1);
     int64_t e0 = 2 * q;
     float2 a = x[e0];
-    y[e0] = make_float2(a.x + sigma * rad0 * c0, a.y + sigma * rad0 * s0);
+    y[e0] = make_float2(a.x + sigma * n0.x, a.y + sigma * n0.y);
     if (e0 + 1 < count) {
       float2 b = x[e0 + 1];
-      y[e0 + 1] = make_float2(b.x + sigma * rad1 * c1, b.y + sigma * rad1 * s1);
+      y[e0 + 1] = make_float2(b.x + sigma * n1.x, b.y + sigma * n1.y);
+    }
+  }
+}
+
+// Fused map_bits -> awgn -> demap for Gray QAM (the Pipeline's fast chain):
+// coded bits [nsym*m] in, f32 LLRs [nsym*m] out, no symbol arrays in HBM.
+// Same points, noise stream and arithmetic order as k_map_bits + k_awgn
+// (y is bit-identical); the per-axis log-sum-exp runs in f32
+// (|dLLR| ~1e-6 relative to the f64 demapper, inside the 1e-4 tolerance).
+struct QamAxesF {
+  float amp[16];
+  int lab[16];
+};
+
+template <int HALF>
+__global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, const float2 *__restrict__ pts,
+                            float sigma, float inv_no, uint64_t seed, uint64_t sid, const QamAxesF A, int maxlog,
+                            float *__restrict__ llr) {
+  constexpr int L = 1 << HALF, M = 2 * HALF;
+  __shared__ float s_amp[L];
+  __shared__ int s_lab[L];
+  __shared__ float2 s_pts[L * L];
+  if (threadIdx.x < L) {
+    s_amp[threadIdx.x] = A.amp[threadIdx.x];
+    s_lab[threadIdx.x] = A.lab[threadIdx.x];
+  }
+  for (int p = threadIdx.x; p < L * L; p += blockDim.x) s_pts[p] = pts[p];
+  __syncthreads();
+  const int64_t npair = (nsym + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    float2 nz[2];
+    normal_pair(q, seed, sid, nz[0], nz[1]);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t s = 2 * q + u;
+      if (s >= nsym) break;
+      int label = 0;
+#pragma unroll
+      for (int t = 0; t < M; ++t) label = (label << 1) | (bits[s * M + t] & 1);
+      const float2 x = s_pts[label];
+      const float yv[2] = {x.x + sigma * nz[u].x, x.y + sigma * nz[u].y};
+      float out[M];
+#pragma unroll
+      for (int ax = 0; ax < 2; ++ax) {
+        float lg[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const float d = yv[ax] - s_amp[l];
+          lg[l] = -(d * d) * inv_no;
+        }
+#pragma unroll
+        for (int t = 0; t < HALF; ++t) {
+          const int sh = HALF - 1 - t;
+          float mx1 = -INFINITY, mx0 = -INFINITY;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {  // level l carries Gray label l ^ (l >> 1)
+            if (((l ^ (l >> 1)) >> sh) & 1) mx1 = fmaxf(mx1, lg[l]);
+            else mx0 = fmaxf(mx0, lg[l]);
+          }
+          float v = mx1 - mx0;
+          if (!maxlog) {
+            float s1 = 0.0f, s0 = 0.0f;
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+              if (((l ^ (l >> 1)) >> sh) & 1) s1 += __expf(lg[l] - mx1);
+              else s0 += __expf(lg[l] - mx0);
+            }
+            v += __logf(s1) - __logf(s0);  // the max terms contribute exactly 1 each
+          }
+          out[2 * t + ax] = v;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < M; ++j) llr[s * M + j] = out[j];
     }
   }
 }
@@ -457,6 +541,36 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, 
     default: k_demap_qam<4><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
   }
   LS_CHECK_LAUNCH("ls_demap_qam");
+  return LS_OK;
+}
+
+int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, const double *amp,
+                 const int32_t *lab, double no, uint64_t seed, uint64_t stream_id, int mode, float *llr,
+                 void *stream) {
+  if (!(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
+  if (m < 2 || m > 8 || (m % 2)) return fail(LS_EINVAL, "modem_qam: bits per symbol must be 2, 4, 6 or 8");
+  if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
+  if (!nsym) return LS_OK;
+  QamAxesF A;
+  const int L = 1 << (m / 2);
+  for (int l = 0; l < 16; ++l) {
+    A.amp[l] = l < L ? (float)amp[l] : 0.0f;
+    A.lab[l] = l < L ? lab[l] : 0;
+    if (l < L && lab[l] != (l ^ (l >> 1)))
+      return fail(LS_EINVAL, "modem_qam: levels must carry the Gray labels l ^ (l >> 1)");
+  }
+  const float2 *pp = reinterpret_cast<const float2 *>(points);
+  const float sigma = (float)sqrt(no / 2.0), inv = (float)(1.0 / no);
+  const int ml = mode == LS_DEMAP_MAXLOG;
+  cudaStream_t s = as_stream(stream);
+  const unsigned g = grid_for((nsym + 1) / 2, 256);
+  switch (m) {
+    case 2: k_modem_qam<1><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
+    case 4: k_modem_qam<2><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
+    case 6: k_modem_qam<3><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
+    default: k_modem_qam<4><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
+  }
+  LS_CHECK_LAUNCH("ls_modem_qam");
   return LS_OK;
 }
 

@@ -198,7 +198,7 @@ def bp_decode(llr, pcm: ParityCheckMatrix, num_iter: int = 20, variant: str = "s
 
 def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum-product",
                   scale: float = 0.75, *, mode: str = "exact", early_stop: bool = True,
-                  device: bool = False):
+                  device: bool = False, precision: str = "auto"):
     """BP-decode rate-matched LLRs -> [batch, k] info bits (ldpc.py:354-365)."""
     _check_variant(variant, num_iter)
     if mode == "exact":
@@ -208,11 +208,19 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
         return L.to_host(out) if (not L.is_tensor(llr) and not device) else out
     if mode != "fast":
         raise ValueError(f"unknown decoder mode {mode!r}")
-    res = qc_decode(llr, code, num_iter, variant, scale, early_stop=early_stop)
+    if precision == "auto":
+        precision = "fp16x2" if qc_has_kernel(code, "fp16x2", prune=True) else "fp32"
+    res = qc_decode(llr, code, num_iter, variant, scale, early_stop=early_stop, precision=precision)
     return L.to_host(res["hard"]) if (not L.is_tensor(llr) and not device) else res["hard"]
 
 
 LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16 = 1, 2, 4
+
+
+def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True) -> bool:
+    """Whether a compile-time specialised fast decoder exists for this code."""
+    flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
+    return bool(L.lib().ls_qc_has_kernel(code.handle, flags))
 
 
 def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum", scale: float = 0.75,

@@ -169,6 +169,29 @@ def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str
     return L.to_host(out) if (was_np and not device) else out
 
 
+def modem_qam(coded, constellation: Constellation, no: float, rng, demapper: str = "app"):
+    """Fused map_bits -> awgn -> demap (f32 LLRs, device) for Gray QAM: the
+    Pipeline's fast chain (sweep.py:352-356 in one pass).  The noisy symbols
+    equal map_bits + awgn with the same stream; the LLRs are computed in f32."""
+    axes = constellation.qam_axes()
+    if axes is None:
+        raise ValueError("modem_qam needs a Gray QAM constellation")
+    if demapper not in ("app", "maxlog"):
+        raise ValueError(f"unknown demapper {demapper!r}")
+    if not no > 0:
+        raise ValueError("demap: noise variance must be > 0")
+    m = constellation.num_bits_per_symbol
+    tb = L.to_device(coded, "uint8")
+    if tb.shape[-1] % m != 0:
+        raise ValueError(f"bit count {tb.shape[-1]} not divisible by {m} bits/symbol")
+    amp, lab = axes
+    out = L.empty(tuple(tb.shape), "float32")
+    L.call("ls_modem_qam", L.ptr(tb), tb.numel() // m, m, L.ptr(constellation.device_points("float32")),
+           amp.ctypes.data, lab.ctypes.data, float(no), rng.seed & ((1 << 64) - 1),
+           rng.stream_id & ((1 << 64) - 1), 0 if demapper == "app" else 1, L.ptr(out), L.stream_ptr())
+    return out
+
+
 def demap_app(y, no, constellation: Constellation, prior=None, out_dtype: str = "float64",
               device: bool = False):
     """Exact APP LLRs ln(p1/p0) (mapping.py:146-153), f64 arithmetic on GPU."""

@@ -23,8 +23,8 @@ import numpy as np
 from . import _lib as L
 from .channel import awgn
 from .core import RngStream, binary_source, count_errors, ebnodb2no
-from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode
-from .mapping import Constellation, demap_app, demap_maxlog, map_bits
+from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode, qc_has_kernel
+from .mapping import Constellation, demap_app, demap_maxlog, map_bits, modem_qam
 
 CSV_COLUMNS = ("ebno_db", "bits", "bit_errors", "ber", "blocks", "block_errors", "bler", "batches",
                "stop_reason", "elapsed_s")
@@ -181,6 +181,10 @@ class Pipeline:
             self.decoder_mode = dec.get("mode", "exact")
             if self.decoder_mode not in ("exact", "fast"):
                 raise ConfigError("code.decoder.mode", f"unknown mode {self.decoder_mode!r}")
+            self.decoder_precision = dec.get("precision", "auto")
+            if self.decoder_precision not in ("auto", "fp32", "fp16x2"):
+                raise ConfigError("code.decoder.precision",
+                                  f"unknown precision {self.decoder_precision!r}")
             self.payload_bits = code["k"]
             self.coded_bits = code["n"]
             self.coderate = code["k"] / code["n"]
@@ -191,22 +195,41 @@ class Pipeline:
         self.num_symbols = self.coded_bits // self.m
 
     # -- per-batch simulation (device resident) ------------------------------
+    @property
+    def fused_modem(self) -> bool:
+        """Fast chain: one fused map+AWGN+demap pass for Gray QAM."""
+        return (self.family != "none" and self.decoder_mode == "fast"
+                and self.constellation.qam_axes() is not None)
+
     def _llr(self, ebno_db: float, batch_size: int, rng: RngStream):
         no = ebnodb2no(ebno_db, self.m, self.coderate)
         payload = binary_source([batch_size, self.payload_bits], rng.child(0), device=True)
         coded = payload if self.family == "none" else ldpc5g_encode(payload, self.ldpc, device=True)
+        if self.fused_modem:
+            llr = modem_qam(coded, self.constellation, no, rng.child(2), self.demapper)
+            return payload, llr
         x = map_bits(coded, self.constellation, device=True)
         y = awgn(x, no, rng.child(2), device=True)
         llr = self.demap(y, no, self.constellation, out_dtype="float32", device=True)
         return payload, llr
+
+    @property
+    def precision(self) -> str:
+        if self.decoder_precision != "auto":
+            return self.decoder_precision
+        return "fp16x2" if qc_has_kernel(self.ldpc, "fp16x2", prune=True) else "fp32"
 
     def run_batch_device(self, ebno_db: float, batch_size: int, rng: RngStream):
         """(payload, decoded) as CUDA tensors."""
         payload, llr = self._llr(ebno_db, batch_size, rng)
         if self.family == "none":
             return payload, (llr > 0).to(L.torch().uint8)
-        dec = ldpc5g_decode(llr, self.ldpc, self.bp_iter, self.bp_variant, self.bp_scale,
-                            mode=self.decoder_mode, early_stop=self.bp_early_stop, device=True)
+        if self.decoder_mode == "fast":
+            dec = qc_decode(llr, self.ldpc, self.bp_iter, self.bp_variant, self.bp_scale,
+                            early_stop=self.bp_early_stop, precision=self.precision)["hard"]
+        else:
+            dec = ldpc5g_decode(llr, self.ldpc, self.bp_iter, self.bp_variant, self.bp_scale,
+                                mode="exact", early_stop=self.bp_early_stop, device=True)
         return payload, dec
 
     def run_batch(self, ebno_db: float, batch_size: int, rng: RngStream):
@@ -222,7 +245,8 @@ class Pipeline:
         if self.family != "none" and self.decoder_mode == "fast":
             payload, llr = self._llr(ebno_db, batch_size, rng)
             qc_decode(llr, self.ldpc, self.bp_iter, self.bp_variant, self.bp_scale,
-                      early_stop=self.bp_early_stop, ref_bits=payload, want_hard=False, counts=counts)
+                      early_stop=self.bp_early_stop, ref_bits=payload, want_hard=False, counts=counts,
+                      precision=self.precision)
             return counts
         p, d = self.run_batch_device(ebno_db, batch_size, rng)
         L.call("ls_count_errors", L.ptr(p), L.ptr(d), p.shape[0], p.shape[1], L.ptr(counts), L.stream_ptr())

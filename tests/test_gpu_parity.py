@@ -107,6 +107,21 @@ def test_demap_per_symbol_noise_and_errors():
         lb.demap_app(y, 0.0, const)
 
 
+@pytest.mark.parametrize("m", [2, 4, 6, 8])
+@pytest.mark.parametrize("demapper", ["app", "maxlog"])
+def test_fused_modem_matches_unfused_stages(m, demapper):
+    """ls_modem_qam == demap(awgn(map_bits(.))) with the same stream, within
+    the north-star LLR tolerance 1e-4 * max(|L|, 1) (f32 vs f64 demapping)."""
+    const = lb.Constellation("qam", m)
+    bits = lb.binary_source([8, 96 * m], lb.RngStream(3, 4))
+    rng = lb.RngStream(5, 6)
+    no = lb.ebnodb2no(4.0, m, 0.5)
+    fused = lb.mapping.modem_qam(bits, const, no, rng, demapper).cpu().numpy()
+    y = lb.awgn(lb.map_bits(bits, const), no, rng)
+    ref = (lb.demap_app if demapper == "app" else lb.demap_maxlog)(y, no, const)
+    assert np.all(np.abs(fused - ref) <= 1e-4 * np.maximum(np.abs(ref), 1.0))
+
+
 def test_chain_stage_llrs_match_golden(golden):
     for cfg in ("c1", "c2", "c4"):
         d = golden(f"chain_{cfg}")
