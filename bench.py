@@ -257,6 +257,8 @@ def run_b200(a, rank, world, local_rank):
     if not a.no_e2e:
         line["e2e"] = e2e_chain(a, pipe, rank, world, dist)
         line["e2e_decode_only"] = e2e_decode(a, pipe, rank, world, dist)
+    if not a.early_stop:
+        line["early_stop_variant"] = early_stop_rate(a, pipe, rank, world, dist)
     if not a.no_exact and rank == 0:
         line["exact_mode"] = exact_rate(a, pipe)
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -270,6 +272,49 @@ def run_b200(a, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def early_stop_rate(a, pipe, rank, world, dist, steps=3):
+    """Same chain with the syndrome early stop on (max 20 iterations), the
+    second BASELINE.md variant; reports the mean iterations executed."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+    from paper_2203_11854_b200 import _lib as L
+
+    B = a.batch
+    counts = L.zeros((2,), "int64")
+    iters = []
+
+    def one(i):
+        payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (900 + i)))
+        r = lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=True, ref_bits=payload,
+                         want_hard=False, want_iters=True, counts=counts, precision=pipe.precision)
+        iters.append(r["iters"])
+
+    one(-1)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters.clear()
+    counts.zero_()
+    e0.record()
+    for i in range(steps):
+        one(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm[0])
+    mean_it = float(torch.cat(iters).float().mean())
+    c = counts.cpu().tolist()
+    return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s",
+            "mean_iterations": mean_it, "ms_per_step": ms / steps,
+            "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
+            "note": "fp16x2 kernel pairs two codewords per CTA: a pair runs until both converge"}
+
+
 def _wall_max(dist, secs):
     import torch
 
@@ -280,7 +325,7 @@ def _wall_max(dist, secs):
     return float(t[0])
 
 
-def e2e_chain(a, pipe, rank, world, dist, steps=2):
+def e2e_chain(a, pipe, rank, world, dist, steps=3):
     """The public API call a user makes (Pipeline.run_batch, sweep.py:347):
     host numpy (payload, decoded) out every step."""
     import torch
@@ -288,7 +333,10 @@ def e2e_chain(a, pipe, rank, world, dist, steps=2):
     import paper_2203_11854_b200 as lb
 
     B = a.batch
-    pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 99))
+    # two warm-up calls: the caller holds one result while the next is made, so
+    # the pinned-host caching allocator needs two output sets before steady state
+    p, d = pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 98))
+    p, d = pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 99))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -302,7 +350,7 @@ def e2e_chain(a, pipe, rank, world, dist, steps=2):
             "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys"}
 
 
-def e2e_decode(a, pipe, rank, world, dist, steps=2):
+def e2e_decode(a, pipe, rank, world, dist, steps=3):
     """Drop-in decoder with HOST buffers: pinned f32 LLRs in, decoded bits out
     (ldpc5g_decode(llr, code, mode='fast'))."""
     import torch
@@ -315,14 +363,15 @@ def e2e_decode(a, pipe, rank, world, dist, steps=2):
     host.copy_(llr)
     del llr
     out = torch.empty((B, K_INFO), dtype=torch.uint8, pin_memory=True)
-    lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
+    for _ in range(2):
+        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t = time.perf_counter()
     for _ in range(steps):
         dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
-        out.copy_(dec)
+        assert dec.device.type == "cpu" and dec.shape == out.shape  # decoded bits are on the host
     torch.cuda.synchronize()
     el = _wall_max(dist, time.perf_counter() - t)
     return {"value": world * B * K_INFO * steps / el / 1e9, "unit": "Gbit/s",

@@ -112,6 +112,18 @@ int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, 
                  const int32_t *lab, double no, uint64_t seed, uint64_t stream_id, int mode,
                  float *llr, void *stream);
 
+/* Slice variants for chunked (copy-overlapped) batches: the same streams as
+ * one call over the whole array, starting at element `offset` of it
+ * (binary_source: bit offset, multiple of 32; awgn / modem: complex
+ * element / symbol offset, even). */
+int ls_binary_source_at(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count,
+                        uint8_t *bits, void *stream);
+int ls_awgn_at(const float *x, int64_t offset, int64_t count, double no, uint64_t seed,
+               uint64_t stream_id, float *y, void *stream);
+int ls_modem_qam_at(const uint8_t *bits, int64_t offset, int64_t nsym, int m, const float *points,
+                    const double *amp, const int32_t *lab, double no, uint64_t seed,
+                    uint64_t stream_id, int mode, float *llr, void *stream);
+
 /* ---- LDPC ------------------------------------------------------------ */
 /* ldpc5g_encode(bits, code) (ldpc.py:298-351): bits [B,k] -> rate-matched
  * codewords tx [B,n] (nullable) and/or the mother codeword full [B,n_full]

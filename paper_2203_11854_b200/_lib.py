@@ -39,6 +39,9 @@ _SIGS = {
     "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_modem_qam": [_vp, _i64, _int, _vp, _vp, _vp, _dbl, _u64, _u64, _int, _vp, _vp],
+    "ls_binary_source_at": [_u64, _u64, _i64, _i64, _vp, _vp],
+    "ls_awgn_at": [_vp, _i64, _i64, _dbl, _u64, _u64, _vp, _vp],
+    "ls_modem_qam_at": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _dbl, _u64, _u64, _int, _vp, _vp],
     "ls_encode": [_vp, _vp, _i64, _vp, _vp, _vp],
     "ls_derate": [_vp, _vp, _int, _i64, _vp, _vp],
     "ls_bp_decode": [_vp, _vp, _int, _i64, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp],

@@ -16,15 +16,16 @@ from .core import RngStream
 _MASK64 = (1 << 64) - 1
 
 
-def awgn(x, no: float, rng: RngStream, device: bool = False):
-    """x + CN(0, no) per element (channel.py:33-40); complex64 arithmetic."""
+def awgn(x, no: float, rng: RngStream, device: bool = False, offset: int = 0):
+    """x + CN(0, no) per element (channel.py:33-40); complex64 arithmetic.
+    `offset` (even) = index of x's first element in the full stream."""
     if no < 0:
         raise ValueError(f"noise variance must be >= 0, got {no}")
     was_np = not L.is_tensor(x)
     tx = L.to_device(x, "complex64")
     out = L.empty(tx.shape, "complex64")
-    L.call("ls_awgn", L.ptr(tx), tx.numel(), float(no), rng.seed & _MASK64, rng.stream_id & _MASK64,
-           L.ptr(out), L.stream_ptr())
+    L.call("ls_awgn_at", L.ptr(tx), int(offset), tx.numel(), float(no), rng.seed & _MASK64,
+           rng.stream_id & _MASK64, L.ptr(out), L.stream_ptr())
     return L.to_host(out) if (was_np and not device) else out
 
 

@@ -50,15 +50,16 @@ def _shape(shape):
     return shape
 
 
-def binary_source(shape, rng: RngStream, device: bool = False):
+def binary_source(shape, rng: RngStream, device: bool = False, offset: int = 0):
     """i.i.d. bits (core.py:47-54), bit-exact with the reference's draws.
 
     Returns numpy uint8 like the reference; `device=True` returns the CUDA
-    tensor instead (no host copy).
+    tensor instead (no host copy).  `offset` (a multiple of 32) starts the
+    draw at that bit of the stream, for row chunks of a larger batch.
     """
     shape = _shape(shape)
     out = L.empty(shape, "uint8")
-    L.call("ls_binary_source", rng.seed & _MASK64, rng.stream_id & _MASK64, out.numel(),
+    L.call("ls_binary_source_at", rng.seed & _MASK64, rng.stream_id & _MASK64, int(offset), out.numel(),
            L.ptr(out), L.stream_ptr())
     return out if device else L.to_host(out)
 

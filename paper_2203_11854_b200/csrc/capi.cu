@@ -28,12 +28,15 @@ int cuda_status(cudaError_t e, const char *where) {
 // One thread per Philox block = 4 uint64 words = 32 payload bits.  Bit j of
 // word w is (w >> (8j+7)) & 1: low uint32 half first, bytes LSB first, each
 // bit the byte's MSB (numpy bounded uint8 draw).
-__global__ void k_binary_source(uint64_t seed, uint64_t sid, int64_t count, uint8_t *__restrict__ bits) {
+// `blk0` = index of the first Philox block (32 bits each) of this slice of
+// the stream, so a [B, k] draw can be produced in row chunks.
+__global__ void k_binary_source(uint64_t seed, uint64_t sid, int64_t blk0, int64_t count,
+                                uint8_t *__restrict__ bits) {
   const int64_t nblk = (count + 31) / 32;
   for (int64_t blk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; blk < nblk;
        blk += (int64_t)gridDim.x * blockDim.x) {
     uint64_t w[4];
-    philox4x64_10((uint64_t)blk + 1, 0, 0, 0, sid, seed, w);
+    philox4x64_10((uint64_t)(blk0 + blk) + 1, 0, 0, 0, sid, seed, w);
     const int64_t base = blk * 32;
     if (base + 32 <= count && ((reinterpret_cast<uintptr_t>(bits + base) & 15) == 0)) {
       uint32_t o[8];
@@ -86,12 +89,12 @@ __device__ __forceinline__ void normal_pair(int64_t q, uint64_t seed, uint64_t s
 }
 
 __global__ void k_awgn(const float2 *__restrict__ x, int64_t count, float sigma, uint64_t seed,
-                       uint64_t sid, float2 *__restrict__ y) {
+                       uint64_t sid, int64_t q0, float2 *__restrict__ y) {
   const int64_t npair = (count + 1) / 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
        q += (int64_t)gridDim.x * blockDim.x) {
     float2 n0, n1;
-    normal_pair(q, seed, sid, n0, n1);
+    normal_pair(q0 + q, seed, sid, n0, n1);
     int64_t e0 = 2 * q;
     float2 a = x[e0];
     y[e0] = make_float2(a.x + sigma * n0.x, a.y + sigma * n0.y);
@@ -114,8 +117,8 @@ struct QamAxesF {
 
 template <int HALF>
 __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, const float2 *__restrict__ pts,
-                            float sigma, float inv_no, uint64_t seed, uint64_t sid, const QamAxesF A, int maxlog,
-                            float *__restrict__ llr) {
+                            float sigma, float inv_no, uint64_t seed, uint64_t sid, int64_t q0, const QamAxesF A,
+                            int maxlog, float *__restrict__ llr) {
   constexpr int L = 1 << HALF, M = 2 * HALF;
   __shared__ float s_amp[L];
   __shared__ int s_lab[L];
@@ -130,7 +133,7 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
        q += (int64_t)gridDim.x * blockDim.x) {
     float2 nz[2];
-    normal_pair(q, seed, sid, nz[0], nz[1]);
+    normal_pair(q0 + q, seed, sid, nz[0], nz[1]);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t s = 2 * q + u;
@@ -364,6 +367,147 @@ __global__ void k_encode(QcParams P, const uint8_t *__restrict__ bits, uint8_t *
   }
 }
 
+// ------------------------------------------------------------ bit-packed encoder
+// Same algebra as k_encode, 32 circulant lanes per 32-bit word: a circulant
+// with shift s maps word w of the output to the 32 input bits starting at
+// bit 32w + s of a "doubled" copy of the input vector (bit j = x[j mod Z]),
+// i.e. one funnel shift per (row, word, entry).  One CTA per codeword.
+constexpr int kEncW = 12;            // max words per circulant vector (Z <= 384)
+constexpr int kEncD = 2 * kEncW + 2;  // words of a doubled vector
+
+__device__ __forceinline__ uint32_t bits_at(const uint32_t *a, int pos) {
+  return __funnelshift_r(a[pos >> 5], a[(pos >> 5) + 1], pos & 31);
+}
+
+// 32 bits x[(off + b) mod Z], b = 0..31, of the Z-bit vector starting at bit
+// `base` of the packed array a
+__device__ __forceinline__ uint32_t bits_wrapped(const uint32_t *a, int base, int Z, int off) {
+  int o = off % Z, filled = 0;
+  uint32_t out = 0;
+  while (filled < 32) {
+    const int take = min(32 - filled, Z - o);
+    uint32_t v = bits_at(a, base + o);
+    if (take < 32) v &= (1u << take) - 1u;
+    out |= v << filled;
+    filled += take;
+    o = 0;
+  }
+  return out;
+}
+
+template <class G>
+__global__ void __launch_bounds__(128) k_encode_packed(QcParams P, const uint8_t *__restrict__ bits,
+                                                       uint8_t *__restrict__ tx, uint8_t *__restrict__ full) {
+  constexpr int KB = G::KB, MB = G::MB;
+  __shared__ uint32_t flat[(KB * 384) / 32 + 2];  // systematic bits, flat
+  __shared__ uint32_t xd[KB][kEncD];               // doubled systematic columns
+  __shared__ uint32_t syn[MB][kEncW];              // syndromes, then extension parities
+  __shared__ uint32_t core[4][kEncW + 1];
+  __shared__ uint32_t cored[4][kEncD];
+  __shared__ uint32_t tmpd[kEncD];
+  const int Z = P.z, W = (Z + 31) >> 5, D = 2 * W + 2, t = threadIdx.x, NT = blockDim.x;
+  const uint32_t lastmask = (Z & 31) ? ((1u << (Z & 31)) - 1u) : 0xFFFFFFFFu;
+  const int64_t b = blockIdx.x;
+  const uint8_t *in = bits + b * (int64_t)P.k;
+  const int nflat = (P.k_full + 31) >> 5;
+  // 1. pack the payload (fillers are zero)
+  for (int f = t; f < nflat + 2; f += NT) {
+    uint32_t w = 0;
+    const int j0 = f << 5;
+    if (j0 + 32 <= P.k && ((reinterpret_cast<uintptr_t>(in + j0) & 15) == 0)) {
+      const uint4 a = *reinterpret_cast<const uint4 *>(in + j0);
+      const uint4 c = *reinterpret_cast<const uint4 *>(in + j0 + 16);
+      const uint32_t q[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t v = q[k] & 0x01010101u;  // one bit per byte
+        w |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * k);
+      }
+    } else {
+      for (int e = 0; e < 32; ++e) {
+        const int j = j0 + e;
+        if (j < P.k) w |= (uint32_t)(in[j] & 1) << e;
+      }
+    }
+    flat[f] = w;
+  }
+  __syncthreads();
+  // 2. doubled systematic columns
+  for (int x = t; x < KB * D; x += NT) {
+    const int c = x / D, q = x - c * D;
+    xd[c][q] = bits_wrapped(flat, c * Z, Z, 32 * q);
+  }
+  __syncthreads();
+  // 3. syndromes of the systematic part (ldpc.py:308-311)
+  for (int x = t; x < MB * W; x += NT) {
+    const int r = x / W, w = x - r * W;
+    uint32_t acc = 0;
+    for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
+      const int c = G::d_col(e);
+      if (c < KB) acc ^= bits_at(xd[c], 32 * w + P.s[e]);
+    }
+    syn[r][w] = (w == W - 1) ? (acc & lastmask) : acc;
+  }
+  __syncthreads();
+  // 4. accumulate-core solve (ldpc.py:313-320): p1 = roll(ssum, 1)
+  if (t < kEncW) {
+    uint32_t ss = 0;
+    if (t < W) ss = syn[0][t] ^ syn[1][t] ^ syn[2][t] ^ syn[3][t];
+    core[0][t] = ss;  // ssum staged in core[0]
+  }
+  __syncthreads();
+  for (int q = t; q < D; q += NT) tmpd[q] = bits_wrapped(core[0], 0, Z, 32 * q);
+  __syncthreads();
+  if (t < W) {
+    const uint32_t m = (t == W - 1) ? lastmask : 0xFFFFFFFFu;
+    const uint32_t ss = core[0][t];
+    const uint32_t p1 = bits_at(tmpd, 32 * t + Z - 1) & m;
+    const uint32_t p2 = syn[0][t] ^ ss, p3 = syn[1][t] ^ p1 ^ p2, p4 = syn[2][t] ^ p3;
+    core[0][t] = p1;
+    core[1][t] = p2;
+    core[2][t] = p3;
+    core[3][t] = p4;
+  }
+  __syncthreads();
+  for (int x = t; x < 4 * D; x += NT) {
+    const int cc = x / D, q = x - cc * D;
+    cored[cc][q] = bits_wrapped(core[cc], 0, Z, 32 * q);
+  }
+  __syncthreads();
+  // 5. extension rows (ldpc.py:327-331), in place in syn[r >= 4]
+  for (int x = t; x < (MB - 4) * W; x += NT) {
+    const int r = 4 + x / W, w = x % W;
+    uint32_t acc = syn[r][w];
+    for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
+      const int c = G::d_col(e);
+      if (c >= KB && c < KB + 4) acc ^= bits_at(cored[c - KB], 32 * w + P.s[e]);
+    }
+    syn[r][w] = (w == W - 1) ? (acc & lastmask) : acc;
+  }
+  __syncthreads();
+  // 6. unpack: mother codeword and the rate-matched gather (ldpc.py:351)
+  for (int c = 0; c < G::NB; ++c) {
+    for (int i = t; i < Z; i += NT) {
+      const int v = c * Z + i;
+      uint32_t word;
+      if (c < KB) {
+        const int pos = v;
+        word = bits_at(flat, pos) & 1u;
+      } else if (c < KB + 4) {
+        word = (core[c - KB][i >> 5] >> (i & 31)) & 1u;
+      } else {
+        word = (syn[c - KB][i >> 5] >> (i & 31)) & 1u;
+      }
+      const uint8_t bit = (uint8_t)word;
+      if (full) full[b * (int64_t)P.n_full + v] = bit;
+      if (tx && v >= 2 * Z && !(v >= P.k && v < P.k_full)) {
+        const int pos = v < P.k ? v - 2 * Z : P.l1 + (v - P.k_full);
+        for (int j = pos; j < P.n; j += P.buflen) tx[b * (int64_t)P.n + j] = bit;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ derate_match
 // ldpc.py:335-345: mother = +0.0, np.add.at over transmit_idx in index order,
 // fillers = -40.
@@ -466,13 +610,19 @@ int ls_code_transmit_idx(const ls_code *code, int32_t *host_out) {
   return LS_OK;
 }
 
-int ls_binary_source(uint64_t seed, uint64_t stream_id, int64_t count, uint8_t *bits, void *stream) {
-  if (count < 0 || (!bits && count)) return fail(LS_EINVAL, "binary_source: bad arguments");
+int ls_binary_source_at(uint64_t seed, uint64_t stream_id, int64_t offset, int64_t count, uint8_t *bits,
+                        void *stream) {
+  if (count < 0 || offset < 0 || (!bits && count)) return fail(LS_EINVAL, "binary_source: bad arguments");
+  if (offset % 32) return fail(LS_EINVAL, "binary_source: offset must be a multiple of 32 bits");
   if (!count) return LS_OK;
   const int64_t nblk = (count + 31) / 32;
-  k_binary_source<<<grid_for(nblk, 256), 256, 0, as_stream(stream)>>>(seed, stream_id, count, bits);
+  k_binary_source<<<grid_for(nblk, 256), 256, 0, as_stream(stream)>>>(seed, stream_id, offset / 32, count, bits);
   LS_CHECK_LAUNCH("ls_binary_source");
   return LS_OK;
+}
+
+int ls_binary_source(uint64_t seed, uint64_t stream_id, int64_t count, uint8_t *bits, void *stream) {
+  return ls_binary_source_at(seed, stream_id, 0, count, bits, stream);
 }
 
 int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, float *x, void *stream) {
@@ -484,19 +634,25 @@ int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, f
   return LS_OK;
 }
 
-int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id, float *y,
-            void *stream) {
+int ls_awgn_at(const float *x, int64_t offset, int64_t count, double no, uint64_t seed, uint64_t stream_id,
+               float *y, void *stream) {
   if (no < 0) return fail(LS_EINVAL, "noise variance must be >= 0, got " + std::to_string(no));
+  if (offset < 0 || (offset & 1)) return fail(LS_EINVAL, "awgn: offset must be even and >= 0");
   if (!count) return LS_OK;
   if (no == 0) {
     cudaError_t e = cudaMemcpyAsync(y, x, (size_t)count * 8, cudaMemcpyDeviceToDevice, as_stream(stream));
     return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_awgn");
   }
   k_awgn<<<grid_for((count + 1) / 2, 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float2 *>(x), count, (float)sqrt(no / 2.0), seed, stream_id,
+      reinterpret_cast<const float2 *>(x), count, (float)sqrt(no / 2.0), seed, stream_id, offset / 2,
       reinterpret_cast<float2 *>(y));
   LS_CHECK_LAUNCH("ls_awgn");
   return LS_OK;
+}
+
+int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id, float *y,
+            void *stream) {
+  return ls_awgn_at(x, 0, count, no, seed, stream_id, y, stream);
 }
 
 int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *points64,
@@ -547,7 +703,14 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, 
 int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, const double *amp,
                  const int32_t *lab, double no, uint64_t seed, uint64_t stream_id, int mode, float *llr,
                  void *stream) {
+  return ls_modem_qam_at(bits, 0, nsym, m, points, amp, lab, no, seed, stream_id, mode, llr, stream);
+}
+
+int ls_modem_qam_at(const uint8_t *bits, int64_t offset, int64_t nsym, int m, const float *points,
+                    const double *amp, const int32_t *lab, double no, uint64_t seed, uint64_t stream_id,
+                    int mode, float *llr, void *stream) {
   if (!(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
+  if (offset < 0 || (offset & 1)) return fail(LS_EINVAL, "modem_qam: offset must be even and >= 0");
   if (m < 2 || m > 8 || (m % 2)) return fail(LS_EINVAL, "modem_qam: bits per symbol must be 2, 4, 6 or 8");
   if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
   if (!nsym) return LS_OK;
@@ -564,11 +727,12 @@ int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, 
   const int ml = mode == LS_DEMAP_MAXLOG;
   cudaStream_t s = as_stream(stream);
   const unsigned g = grid_for((nsym + 1) / 2, 256);
+  const int64_t q0 = offset / 2;
   switch (m) {
-    case 2: k_modem_qam<1><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
-    case 4: k_modem_qam<2><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
-    case 6: k_modem_qam<3><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
-    default: k_modem_qam<4><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, A, ml, llr); break;
+    case 2: k_modem_qam<1><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
+    case 4: k_modem_qam<2><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
+    case 6: k_modem_qam<3><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
+    default: k_modem_qam<4><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
   }
   LS_CHECK_LAUNCH("ls_modem_qam");
   return LS_OK;
@@ -579,16 +743,11 @@ int ls_encode(const ls_code *code, const uint8_t *bits, int64_t batch, uint8_t *
   if (!code) return fail(LS_EINVAL, "ls_encode: null code");
   if (!batch) return LS_OK;
   const QcParams &P = code->p;
-  const int threads = std::min(384, ((P.z + 31) / 32) * 32);
-  const size_t smem = (size_t)P.n_full + (size_t)P.mb * P.z;
   cudaStream_t s = as_stream(stream);
-  if (P.bg == 1) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_encode<BG1Tables>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<BG1Tables><<<(unsigned)batch, threads, smem, s>>>(P, bits, tx, full);
-  } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_encode<BG2Tables>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<BG2Tables><<<(unsigned)batch, threads, smem, s>>>(P, bits, tx, full);
-  }
+  if (P.bg == 1)
+    k_encode_packed<BG1Tables><<<(unsigned)batch, 128, 0, s>>>(P, bits, tx, full);
+  else
+    k_encode_packed<BG2Tables><<<(unsigned)batch, 128, 0, s>>>(P, bits, tx, full);
   LS_CHECK_LAUNCH("ls_encode");
   return LS_OK;
 }

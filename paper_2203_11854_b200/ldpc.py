@@ -210,8 +210,43 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
         raise ValueError(f"unknown decoder mode {mode!r}")
     if precision == "auto":
         precision = "fp16x2" if qc_has_kernel(code, "fp16x2", prune=True) else "fp32"
+    host_in = not L.is_tensor(llr) or not llr.is_cuda
+    if host_in and not device:
+        return _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, precision)
     res = qc_decode(llr, code, num_iter, variant, scale, early_stop=early_stop, precision=precision)
     return L.to_host(res["hard"]) if (not L.is_tensor(llr) and not device) else res["hard"]
+
+
+def _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, precision, chunk=8192):
+    """Host LLRs [B, n] -> host bits [B, k]: row chunks copied in on a copy
+    stream, decoded on the compute stream and copied out, so the PCIe
+    transfers overlap the decoder."""
+    torch = L.torch()
+    src = llr if L.is_tensor(llr) else torch.from_numpy(np.ascontiguousarray(np.asarray(llr, np.float32)))
+    if src.dtype != torch.float32:
+        src = src.to(torch.float32)
+    if src.dim() == 1:
+        src = src.unsqueeze(0)
+    if src.shape[-1] != code.n:
+        raise ValueError(f"expected {code.n} LLRs, got {src.shape[-1]}")
+    B = src.shape[0]
+    out = torch.empty((B, code.k), dtype=torch.uint8, pin_memory=True)
+    main = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    dev = L.device()
+    for lo in range(0, B, chunk):
+        hi = min(B, lo + chunk)
+        with torch.cuda.stream(h2d):
+            x = src[lo:hi].to(dev, non_blocking=True)
+        main.wait_stream(h2d)
+        x.record_stream(main)
+        hard = qc_decode(x, code, num_iter, variant, scale, early_stop=early_stop, precision=precision)["hard"]
+        d2h.wait_stream(main)
+        with torch.cuda.stream(d2h):
+            out[lo:hi].copy_(hard, non_blocking=True)
+        hard.record_stream(d2h)
+    d2h.synchronize()
+    return out.numpy() if not L.is_tensor(llr) else out
 
 
 LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16 = 1, 2, 4

@@ -169,7 +169,7 @@ def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str
     return L.to_host(out) if (was_np and not device) else out
 
 
-def modem_qam(coded, constellation: Constellation, no: float, rng, demapper: str = "app"):
+def modem_qam(coded, constellation: Constellation, no: float, rng, demapper: str = "app", offset: int = 0):
     """Fused map_bits -> awgn -> demap (f32 LLRs, device) for Gray QAM: the
     Pipeline's fast chain (sweep.py:352-356 in one pass).  The noisy symbols
     equal map_bits + awgn with the same stream; the LLRs are computed in f32."""
@@ -186,7 +186,8 @@ def modem_qam(coded, constellation: Constellation, no: float, rng, demapper: str
         raise ValueError(f"bit count {tb.shape[-1]} not divisible by {m} bits/symbol")
     amp, lab = axes
     out = L.empty(tuple(tb.shape), "float32")
-    L.call("ls_modem_qam", L.ptr(tb), tb.numel() // m, m, L.ptr(constellation.device_points("float32")),
+    L.call("ls_modem_qam_at", L.ptr(tb), int(offset), tb.numel() // m, m,
+           L.ptr(constellation.device_points("float32")),
            amp.ctypes.data, lab.ctypes.data, float(no), rng.seed & ((1 << 64) - 1),
            rng.stream_id & ((1 << 64) - 1), 0 if demapper == "app" else 1, L.ptr(out), L.stream_ptr())
     return out

@@ -201,15 +201,20 @@ class Pipeline:
         return (self.family != "none" and self.decoder_mode == "fast"
                 and self.constellation.qam_axes() is not None)
 
-    def _llr(self, ebno_db: float, batch_size: int, rng: RngStream):
+    def _llr(self, ebno_db: float, batch_size: int, rng: RngStream, lo: int = 0):
+        """Payload and f32 LLRs of rows [lo, lo + batch_size) of a batch: the
+        random streams are addressed by row, so a batch computed in chunks is
+        identical to one computed at once (lo must be a multiple of 32)."""
         no = ebnodb2no(ebno_db, self.m, self.coderate)
-        payload = binary_source([batch_size, self.payload_bits], rng.child(0), device=True)
+        payload = binary_source([batch_size, self.payload_bits], rng.child(0), device=True,
+                                offset=lo * self.payload_bits)
         coded = payload if self.family == "none" else ldpc5g_encode(payload, self.ldpc, device=True)
+        sym0 = lo * self.num_symbols
         if self.fused_modem:
-            llr = modem_qam(coded, self.constellation, no, rng.child(2), self.demapper)
+            llr = modem_qam(coded, self.constellation, no, rng.child(2), self.demapper, offset=sym0)
             return payload, llr
         x = map_bits(coded, self.constellation, device=True)
-        y = awgn(x, no, rng.child(2), device=True)
+        y = awgn(x, no, rng.child(2), device=True, offset=sym0)
         llr = self.demap(y, no, self.constellation, out_dtype="float32", device=True)
         return payload, llr
 
@@ -219,9 +224,9 @@ class Pipeline:
             return self.decoder_precision
         return "fp16x2" if qc_has_kernel(self.ldpc, "fp16x2", prune=True) else "fp32"
 
-    def run_batch_device(self, ebno_db: float, batch_size: int, rng: RngStream):
-        """(payload, decoded) as CUDA tensors."""
-        payload, llr = self._llr(ebno_db, batch_size, rng)
+    def run_batch_device(self, ebno_db: float, batch_size: int, rng: RngStream, lo: int = 0):
+        """(payload, decoded) as CUDA tensors (rows [lo, lo + batch_size))."""
+        payload, llr = self._llr(ebno_db, batch_size, rng, lo)
         if self.family == "none":
             return payload, (llr > 0).to(L.torch().uint8)
         if self.decoder_mode == "fast":
@@ -232,10 +237,33 @@ class Pipeline:
                                 mode="exact", early_stop=self.bp_early_stop, device=True)
         return payload, dec
 
-    def run_batch(self, ebno_db: float, batch_size: int, rng: RngStream):
-        """Simulate one batch; returns (payload, decoded) numpy bit arrays (sweep.py:347-364)."""
-        p, d = self.run_batch_device(ebno_db, batch_size, rng)
-        return L.to_host(p), L.to_host(d)
+    def run_batch(self, ebno_db: float, batch_size: int, rng: RngStream, chunk: int = 8192):
+        """Simulate one batch; returns (payload, decoded) numpy bit arrays (sweep.py:347-364).
+
+        The batch runs in row chunks; each chunk's results are copied to
+        pinned host memory on a side stream while the next chunk computes.
+        """
+        torch = L.torch()
+        if batch_size <= chunk:
+            p, d = self.run_batch_device(ebno_db, batch_size, rng)
+            return L.to_host(p), L.to_host(d)
+        chunk = max(32, (chunk // 32) * 32)
+        k = self.payload_bits
+        ph = torch.empty((batch_size, k), dtype=torch.uint8, pin_memory=True)
+        dh = torch.empty((batch_size, k), dtype=torch.uint8, pin_memory=True)
+        main = torch.cuda.current_stream()
+        copy = torch.cuda.Stream()
+        for lo in range(0, batch_size, chunk):
+            hi = min(batch_size, lo + chunk)
+            p, d = self.run_batch_device(ebno_db, hi - lo, rng, lo)
+            copy.wait_stream(main)
+            with torch.cuda.stream(copy):
+                ph[lo:hi].copy_(p, non_blocking=True)
+                dh[lo:hi].copy_(d, non_blocking=True)
+            p.record_stream(copy)
+            d.record_stream(copy)
+        copy.synchronize()
+        return ph.numpy(), dh.numpy()
 
     def run_batch_counts(self, ebno_db: float, batch_size: int, rng: RngStream, counts=None):
         """Enqueue one batch and accumulate (bit_errors, block_errors) into the
