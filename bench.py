@@ -363,7 +363,7 @@ def e2e_decode(a, pipe, rank, world, dist, steps=3):
     host.copy_(llr)
     del llr
     out = torch.empty((B, K_INFO), dtype=torch.uint8, pin_memory=True)
-    for _ in range(2):
+    for _ in range(3):  # steady state of the pinned-host caching allocator
         dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
     torch.cuda.synchronize()
     if dist:
@@ -386,7 +386,8 @@ def exact_rate(a, pipe, B=1024):
     import paper_2203_11854_b200 as lb
 
     _, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, 55))
-    lb.ldpc5g_decode(llr[:64], pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
+    for _ in range(2):  # same batch size, so the workspace pool is warm
+        lb.ldpc5g_decode(llr, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
