@@ -88,6 +88,16 @@ int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, f
 int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id, float *y,
             void *stream);
 
+/* Bit-exact replicas of the reference's numpy draws (channel.py:24-40):
+ * ls_standard_normal = `count` draws of Generator.standard_normal on
+ * RngStream(seed, stream_id) (numpy 2.3.5 ziggurat, f64);
+ * ls_awgn_numpy = awgn(x, no, rng) for complex64 x with exactly the
+ * reference's noise: real parts = normals [0, count), imaginary parts =
+ * normals [count, 2*count), scaled by sqrt(no/2) in f64, cast to f32, added. */
+int ls_standard_normal(uint64_t seed, uint64_t stream_id, int64_t count, double *out, void *stream);
+int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
+                  float *y, void *stream);
+
 /* demap_app / demap_maxlog (mapping.py:110-158) without priors for QAM/PSK
  * points: y complex64 [nsym], scalar no (>0) or per-symbol `no_vec` (nullable),
  * f64 log-domain arithmetic; llr written as f32 (`llr32`) or f64 (`llr64`),

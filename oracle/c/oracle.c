@@ -86,6 +86,63 @@ void orc_binary_source(uint64_t seed, uint64_t stream_id, int64_t count, uint8_t
 }
 
 /* ------------------------------------------------------------------ */
+/* Generator.standard_normal: numpy's 256-level ziggurat on next_uint64 */
+/* (numpy/random/src/distributions/distributions.c)       */
+/* ------------------------------------------------------------------ */
+#include "ziggurat_tables.h"
+
+typedef struct {
+    uint64_t seed, sid, pos; /* next word index of the stream */
+    uint64_t blk[4];
+    uint64_t blk_id; /* Philox block held in blk, 0 = none */
+} raw_stream;
+
+static uint64_t next_u64(raw_stream *s) {
+    uint64_t b = s->pos / 4 + 1;
+    if (s->blk_id != b) {
+        uint64_t key[2] = {s->sid, s->seed};
+        uint64_t ctr[4] = {b, 0, 0, 0};
+        philox4x64_10(ctr, key, s->blk);
+        s->blk_id = b;
+    }
+    return s->blk[s->pos++ % 4];
+}
+
+static double next_double(raw_stream *s) { return (double)(next_u64(s) >> 11) * (1.0 / 9007199254740992.0); }
+
+static double zig_normal(raw_stream *s) {
+    for (;;) {
+        uint64_t r = next_u64(s);
+        int idx = (int)(r & 0xff);
+        r >>= 8;
+        int sign = (int)(r & 0x1);
+        uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        double x = (double)rabs * ls_zig_wi[idx];
+        if (sign & 0x1) x = -x;
+        if (rabs < ls_zig_ki[idx]) return x;
+        if (idx == 0) {
+            for (;;) {
+                double xx = -LS_ZIG_INV_R * log1p(-next_double(s));
+                double yy = -log1p(-next_double(s));
+                if (yy + yy > xx * xx)
+                    return ((rabs >> 8) & 0x1) ? -(LS_ZIG_R + xx) : LS_ZIG_R + xx;
+            }
+        } else {
+            if (((ls_zig_fi[idx - 1] - ls_zig_fi[idx]) * next_double(s) + ls_zig_fi[idx]) < exp(-0.5 * x * x))
+                return x;
+        }
+    }
+}
+
+/* count standard normals of RngStream(seed, stream_id), in draw order;
+ * returns the number of uint64 words consumed */
+int64_t orc_standard_normal(uint64_t seed, uint64_t stream_id, int64_t count, double *out) {
+    raw_stream s = {seed, stream_id, 0, {0, 0, 0, 0}, 0};
+    for (int64_t i = 0; i < count; ++i) out[i] = zig_normal(&s);
+    return (int64_t)s.pos;
+}
+
+/* ------------------------------------------------------------------ */
 /* numpy pairwise summation and reduceat segment sums                  */
 /* ------------------------------------------------------------------ */
 static double pairwise_d(const double *x, int64_t n) {

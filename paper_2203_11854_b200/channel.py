@@ -1,10 +1,15 @@
 """Drop-in mirror of the AWGN part of linksim.channel (channel.py:24-40).
 
-The noise is drawn on the GPU from a counter-based Philox4x32-10 stream keyed
-by the RngStream (seed, stream_id): reproducible for any device count and
-statistically equivalent to the reference's numpy ziggurat draws (the
-bit-exact ziggurat replica is SURVEY.md 8f item 2).  Fading/TDL/CIR channels
-are outside the hot path.
+Two noise generators, both on the GPU and both keyed by the RngStream:
+  * noise="numpy" (default): a bit-exact replica of the reference's draws --
+    numpy's Philox4x64-10 stream fed through numpy 2.3.5's 256-level ziggurat
+    (SURVEY.md A3/A4), resolved in parallel despite the data-dependent word
+    consumption (csrc/rng_normal.cu).  awgn() returns exactly the reference's
+    complex64 output.
+  * noise="philox": counter-based Philox4x32-10 + Box-Muller, addressable
+    per element (chunkable, fusable with the mapper/demapper); statistically
+    equivalent.  The sweep engine's fast mode uses it.
+Fading/TDL/CIR channels are outside the hot path.
 """
 from __future__ import annotations
 
@@ -14,26 +19,44 @@ from . import _lib as L
 from .core import RngStream
 
 _MASK64 = (1 << 64) - 1
+NOISE_KINDS = ("numpy", "philox")
 
 
-def awgn(x, no: float, rng: RngStream, device: bool = False, offset: int = 0):
+def awgn(x, no: float, rng: RngStream, device: bool = False, offset: int = 0, noise: str = "numpy"):
     """x + CN(0, no) per element (channel.py:33-40); complex64 arithmetic.
-    `offset` (even) = index of x's first element in the full stream."""
+    `offset` (even, philox noise only) = index of x's first element in the
+    full stream."""
     if no < 0:
         raise ValueError(f"noise variance must be >= 0, got {no}")
+    if noise not in NOISE_KINDS:
+        raise ValueError(f"unknown noise generator {noise!r}")
     was_np = not L.is_tensor(x)
     tx = L.to_device(x, "complex64")
     out = L.empty(tx.shape, "complex64")
-    L.call("ls_awgn_at", L.ptr(tx), int(offset), tx.numel(), float(no), rng.seed & _MASK64,
-           rng.stream_id & _MASK64, L.ptr(out), L.stream_ptr())
+    if noise == "numpy":
+        if offset:
+            raise ValueError("awgn: the numpy-exact stream is drawn for the whole array (offset=0)")
+        L.call("ls_awgn_numpy", L.ptr(tx), tx.numel(), float(no), rng.seed & _MASK64,
+               rng.stream_id & _MASK64, L.ptr(out), L.stream_ptr())
+    else:
+        L.call("ls_awgn_at", L.ptr(tx), int(offset), tx.numel(), float(no), rng.seed & _MASK64,
+               rng.stream_id & _MASK64, L.ptr(out), L.stream_ptr())
     return L.to_host(out) if (was_np and not device) else out
 
 
+def standard_normal(count: int, rng: RngStream, device: bool = False):
+    """`count` draws of rng.generator().standard_normal (f64), bit-exact."""
+    out = L.empty((int(count),), "float64")
+    L.call("ls_standard_normal", rng.seed & _MASK64, rng.stream_id & _MASK64, int(count), L.ptr(out),
+           L.stream_ptr())
+    return out if device else L.to_host(out)
+
+
 def complex_gaussian(shape, rng: RngStream, variance: float = 1.0, dtype=np.complex64,
-                     device: bool = False):
+                     device: bool = False, noise: str = "numpy"):
     """Circularly-symmetric complex Gaussian draws (channel.py:24-30)."""
     if np.dtype(dtype) != np.complex64:
         raise ValueError("complex_gaussian: the B200 path produces complex64")
     zeros = L.zeros(tuple(int(s) for s in np.atleast_1d(shape)), "complex64")
-    return awgn(zeros, variance, rng, device=True) if device else L.to_host(
-        awgn(zeros, variance, rng, device=True))
+    z = awgn(zeros, variance, rng, device=True, noise=noise)
+    return z if device else L.to_host(z)

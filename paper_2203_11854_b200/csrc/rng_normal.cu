@@ -1,0 +1,323 @@
+// Bit-exact GPU replica of numpy's Generator.standard_normal on the
+// RngStream Philox4x64-10 stream (channel.py:24-30 draws):
+// the 256-level ziggurat on next_uint64, with numpy 2.3.5's tables.
+//
+// A normal consumes a data-dependent number of words (1 on the fast path,
+// 99.2 % of draws; more on the wedge / tail paths), so draw j starts at a
+// position that depends on every earlier draw.  The stream is cut into
+// segments of G words and resolved in parallel:
+//   1. per segment: the word lengths of every possible draw start, the rare
+//      multi-word ("special") starts, and a transfer function
+//        entry offset e in [0, K) -> (exit offset into the next segment,
+//                                     number of draws starting in the segment)
+//   2. a two-level scan composes the transfer functions (groups of segments,
+//      then the groups) -> each segment's true entry offset and draw base;
+//   3. per segment: every start position gets its draw index and evaluates
+//      its normal.
+// Only the special positions need sequential treatment, and there are ~8 of
+// them per 1024 words.
+#include <math.h>
+
+#include <algorithm>
+
+#define LS_ZIG_QUAL static __constant__
+#include "common.cuh"
+#include "ziggurat_tables.h"
+
+namespace lsb {
+
+constexpr int kZG = 1024;     // words per segment
+constexpr int kZK = 32;       // entry offsets tracked per segment
+constexpr int kZSpec = 96;    // max multi-word starts per segment
+constexpr int kZGroup = 512;  // segments per scan group
+
+__device__ __forceinline__ uint64_t word_at(uint64_t seed, uint64_t sid, int64_t p) {
+  uint64_t w[4];
+  philox4x64_10((uint64_t)(p >> 2) + 1, 0, 0, 0, sid, seed, w);
+  return w[p & 3];
+}
+
+__device__ __forceinline__ double dbl_at(uint64_t seed, uint64_t sid, int64_t p) {
+  return (double)(word_at(seed, sid, p) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// draw starting at word p: value and number of words consumed
+__device__ double zig_draw(uint64_t seed, uint64_t sid, int64_t p, int *len) {
+  const int64_t p0 = p;
+  for (;;) {
+    uint64_t r = word_at(seed, sid, p++);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = (double)rabs * ls_zig_wi[idx];
+    if (sign & 0x1) x = -x;
+    if (rabs < ls_zig_ki[idx]) {
+      *len = (int)(p - p0);
+      return x;
+    }
+    if (idx == 0) {
+      for (;;) {
+        const double xx = -LS_ZIG_INV_R * log1p(-dbl_at(seed, sid, p++));
+        const double yy = -log1p(-dbl_at(seed, sid, p++));
+        if (yy + yy > xx * xx) {
+          *len = (int)(p - p0);
+          return ((rabs >> 8) & 0x1) ? -(LS_ZIG_R + xx) : LS_ZIG_R + xx;
+        }
+      }
+    } else {
+      const double u = dbl_at(seed, sid, p++);
+      if (((ls_zig_fi[idx - 1] - ls_zig_fi[idx]) * u + ls_zig_fi[idx]) < exp(-0.5 * x * x)) {
+        *len = (int)(p - p0);
+        return x;
+      }
+    }
+  }
+}
+
+// specials of segment s (sorted by position), shared by the segment kernels
+__device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *spos, uint16_t *slen,
+                            int *count, int *overflow) {
+  const int t = threadIdx.x;
+  if (t == 0) *count = 0;
+  __syncthreads();
+  const int64_t base = s * kZG;
+  for (int b = t; b < kZG / 4; b += blockDim.x) {
+    uint64_t w[4];
+    philox4x64_10((uint64_t)((base >> 2) + b) + 1, 0, 0, 0, sid, seed, w);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t r = w[u] >> 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      if (!(rabs < ls_zig_ki[w[u] & 0xff])) {
+        int len;
+        zig_draw(seed, sid, base + 4 * b + u, &len);
+        const int k = atomicAdd(count, 1);
+        if (k < kZSpec) {
+          spos[k] = (uint16_t)(4 * b + u);
+          slen[k] = (uint16_t)min(len, 65535);
+        } else {
+          *overflow = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int n = min(*count, kZSpec);
+  if (t == 0) {  // insertion sort, ~8 entries
+    for (int i = 1; i < n; ++i) {
+      const uint16_t p = spos[i], l = slen[i];
+      int j = i - 1;
+      while (j >= 0 && spos[j] > p) {
+        spos[j + 1] = spos[j];
+        slen[j + 1] = slen[j];
+        --j;
+      }
+      spos[j + 1] = p;
+      slen[j + 1] = l;
+    }
+  }
+  __syncthreads();
+  return n;
+}
+
+// walk the specials from entry e: number of draw starts before position `upto`
+// and the next start position `cur` (>= upto means upto is not a start)
+__device__ __forceinline__ void zig_walk(const uint16_t *spos, const uint16_t *slen, int n, int e, int upto,
+                                         int *cnt_out, int *cur_out) {
+  int cur = e, cnt = 0;
+  for (int i = 0; i < n; ++i) {
+    const int q = spos[i];
+    if (q >= upto) break;
+    if (q >= cur) {
+      cnt += q - cur + 1;
+      cur = q + slen[i];
+    }
+  }
+  *cnt_out = cnt;
+  *cur_out = cur;
+}
+
+__global__ void k_zig_segments(uint64_t seed, uint64_t sid, int64_t nseg, uint32_t *__restrict__ trans,
+                               int *__restrict__ overflow) {
+  __shared__ uint16_t spos[kZSpec], slen[kZSpec];
+  __shared__ int count;
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const int n = zig_specials(seed, sid, s, spos, slen, &count, overflow);
+    const int e = threadIdx.x;
+    if (e < kZK) {
+      int cnt, cur;
+      zig_walk(spos, slen, n, e, kZG, &cnt, &cur);
+      if (cur < kZG) {
+        cnt += kZG - cur;
+        cur = kZG;
+      }
+      const int ex = cur - kZG;
+      if (ex >= kZK) *overflow = 1;
+      trans[s * kZK + e] = (uint32_t)cnt | ((uint32_t)min(ex, kZK - 1) << 16);
+    }
+    __syncthreads();
+  }
+}
+
+// compose the transfer functions of each group of kZGroup segments; thread = entry
+__global__ void k_zig_groups(const uint32_t *__restrict__ trans, int64_t nseg, uint32_t *__restrict__ gexit,
+                             int64_t *__restrict__ gcnt) {
+  const int64_t g = blockIdx.x;
+  const int e = threadIdx.x;
+  if (e >= kZK) return;
+  int cur = e;
+  int64_t tot = 0;
+  const int64_t s0 = g * kZGroup, s1 = (s0 + kZGroup < nseg) ? s0 + kZGroup : nseg;
+  for (int64_t s = s0; s < s1; ++s) {
+    const uint32_t t = trans[s * kZK + cur];
+    tot += t & 0xFFFFu;
+    cur = (int)(t >> 16);
+  }
+  gexit[g * kZK + e] = (uint32_t)cur;
+  gcnt[g * kZK + e] = tot;
+}
+
+__global__ void k_zig_top(const uint32_t *__restrict__ gexit, const int64_t *__restrict__ gcnt, int64_t ngroups,
+                          int *__restrict__ gentry, int64_t *__restrict__ gbase, int64_t *__restrict__ total) {
+  int cur = 0;
+  int64_t base = 0;
+  for (int64_t g = 0; g < ngroups; ++g) {
+    gentry[g] = cur;
+    gbase[g] = base;
+    base += gcnt[g * kZK + cur];
+    cur = (int)gexit[g * kZK + cur];
+  }
+  *total = base;
+}
+
+__global__ void k_zig_assign(const uint32_t *__restrict__ trans, int64_t nseg, int64_t ngroups,
+                             const int *__restrict__ gentry, const int64_t *__restrict__ gbase,
+                             int *__restrict__ sentry, int64_t *__restrict__ sbase) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  int cur = gentry[g];
+  int64_t base = gbase[g];
+  const int64_t s0 = g * kZGroup, s1 = (s0 + kZGroup < nseg) ? s0 + kZGroup : nseg;
+  for (int64_t s = s0; s < s1; ++s) {
+    sentry[s] = cur;
+    sbase[s] = base;
+    const uint32_t t = trans[s * kZK + cur];
+    base += t & 0xFFFFu;
+    cur = (int)(t >> 16);
+  }
+}
+
+__global__ void k_zig_emit(uint64_t seed, uint64_t sid, int64_t nseg, const int *__restrict__ sentry,
+                           const int64_t *__restrict__ sbase, int64_t count, double *__restrict__ out,
+                           int *__restrict__ overflow) {
+  __shared__ uint16_t spos[kZSpec], slen[kZSpec];
+  __shared__ int cnt_s;
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const int64_t base = sbase[s];
+    if (base >= count) continue;  // uniform per block
+    const int n = zig_specials(seed, sid, s, spos, slen, &cnt_s, overflow);
+    const int e = sentry[s];
+    for (int p = threadIdx.x; p < kZG; p += blockDim.x) {
+      if (p < e) continue;
+      int cnt, cur;
+      zig_walk(spos, slen, n, e, p, &cnt, &cur);
+      if (p < cur) continue;  // consumed by an earlier multi-word draw
+      const int64_t j = base + cnt + (p - cur);
+      if (j < count) {
+        int len;
+        out[j] = zig_draw(seed, sid, s * kZG + p, &len);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// y = x + f32(sqrt(no/2) * z): re from normal e, im from normal S + e
+// (complex_gaussian draws all real parts, then all imaginary parts)
+__global__ void k_awgn_apply(const float2 *__restrict__ x, int64_t S, double scale, const double *__restrict__ z,
+                             float2 *__restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S; e += (int64_t)gridDim.x * blockDim.x) {
+    const float2 a = x[e];
+    const float nr = (float)(scale * z[e]), ni = (float)(scale * z[S + e]);
+    y[e] = make_float2(a.x + nr, a.y + ni);
+  }
+}
+
+static int normals(uint64_t seed, uint64_t sid, int64_t count, double *out, cudaStream_t s) {
+  const int64_t words = (int64_t)((double)count * 1.06) + 8 * kZG;
+  const int64_t nseg = (words + kZG - 1) / kZG;
+  const int64_t ngroups = (nseg + kZGroup - 1) / kZGroup;
+  char *ws = nullptr;
+  const size_t sz_trans = sizeof(uint32_t) * nseg * kZK, sz_gx = sizeof(uint32_t) * ngroups * kZK,
+               sz_gc = sizeof(int64_t) * ngroups * kZK, sz_ge = sizeof(int) * ngroups,
+               sz_gb = sizeof(int64_t) * ngroups, sz_se = sizeof(int) * nseg, sz_sb = sizeof(int64_t) * nseg;
+  const size_t total = sz_trans + sz_gx + sz_gc + sz_ge + sz_gb + sz_se + sz_sb + 64;
+  cudaError_t e = cudaMallocAsync((void **)&ws, total, s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_standard_normal(workspace)");
+  char *p = ws;
+  auto take = [&](size_t n) {
+    char *q = p;
+    p += (n + 15) & ~size_t(15);
+    return q;
+  };
+  uint32_t *trans = (uint32_t *)take(sz_trans);
+  uint32_t *gexit = (uint32_t *)take(sz_gx);
+  int64_t *gcnt = (int64_t *)take(sz_gc);
+  int *gentry = (int *)take(sz_ge);
+  int64_t *gbase = (int64_t *)take(sz_gb);
+  int *sentry = (int *)take(sz_se);
+  int64_t *sbase = (int64_t *)take(sz_sb);
+  int *flags = (int *)take(16);
+  int64_t *avail = (int64_t *)(flags + 2);
+  cudaMemsetAsync(flags, 0, 16, s);
+  const unsigned gs = (unsigned)std::min<int64_t>(nseg, 148 * 16);
+  k_zig_segments<<<gs, 256, 0, s>>>(seed, sid, nseg, trans, flags);
+  k_zig_groups<<<(unsigned)ngroups, kZK, 0, s>>>(trans, nseg, gexit, gcnt);
+  k_zig_top<<<1, 1, 0, s>>>(gexit, gcnt, ngroups, gentry, gbase, avail);
+  k_zig_assign<<<grid_for(ngroups, 128), 128, 0, s>>>(trans, nseg, ngroups, gentry, gbase, sentry, sbase);
+  k_zig_emit<<<gs, 256, 0, s>>>(seed, sid, nseg, sentry, sbase, count, out, flags);
+  int hflags[2] = {0, 0};
+  int64_t havail = 0;
+  cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&havail, avail, sizeof(havail), cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_standard_normal");
+  if (hflags[0]) return fail(LS_ECUDA, "ls_standard_normal: ziggurat segment overflow");
+  if (havail < count) return fail(LS_ECUDA, "ls_standard_normal: word budget too small");
+  return LS_OK;
+}
+
+}  // namespace lsb
+
+using namespace lsb;
+
+extern "C" int ls_standard_normal(uint64_t seed, uint64_t stream_id, int64_t count, double *out, void *stream) {
+  if (count < 0 || (count && !out)) return fail(LS_EINVAL, "standard_normal: bad arguments");
+  if (!count) return LS_OK;
+  return normals(seed, stream_id, count, out, as_stream(stream));
+}
+
+extern "C" int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
+                             float *y, void *stream) {
+  if (no < 0) return fail(LS_EINVAL, "noise variance must be >= 0, got " + std::to_string(no));
+  if (!count) return LS_OK;
+  cudaStream_t s = as_stream(stream);
+  if (no == 0) {
+    cudaError_t e = cudaMemcpyAsync(y, x, (size_t)count * 8, cudaMemcpyDeviceToDevice, s);
+    return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_awgn_numpy");
+  }
+  double *z = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&z, sizeof(double) * 2 * count, s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_awgn_numpy(workspace)");
+  int rc = normals(seed, stream_id, 2 * count, z, s);
+  if (rc == LS_OK) {
+    k_awgn_apply<<<grid_for(count, 256), 256, 0, s>>>(reinterpret_cast<const float2 *>(x), count, sqrt(no / 2.0), z,
+                                                      reinterpret_cast<float2 *>(y));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_status(e, "ls_awgn_numpy");
+  }
+  cudaFreeAsync(z, s);
+  return rc;
+}

@@ -193,12 +193,23 @@ class Pipeline:
                               f"coded block of {self.coded_bits} bits is not divisible by "
                               f"{self.m} bits/symbol")
         self.num_symbols = self.coded_bits // self.m
+        _ = self.noise  # validates channel.noise
 
     # -- per-batch simulation (device resident) ------------------------------
     @property
+    def noise(self) -> str:
+        """'numpy' (the reference's exact draws) unless the fast decoder is
+        selected; `channel.noise` overrides."""
+        default = "philox" if (self.family != "none" and self.decoder_mode == "fast") else "numpy"
+        kind = self.cfg.channel.get("noise", default)
+        if kind not in ("numpy", "philox"):
+            raise ConfigError("channel.noise", f"unknown noise generator {kind!r}")
+        return kind
+
+    @property
     def fused_modem(self) -> bool:
         """Fast chain: one fused map+AWGN+demap pass for Gray QAM."""
-        return (self.family != "none" and self.decoder_mode == "fast"
+        return (self.family != "none" and self.decoder_mode == "fast" and self.noise == "philox"
                 and self.constellation.qam_axes() is not None)
 
     def _llr(self, ebno_db: float, batch_size: int, rng: RngStream, lo: int = 0):
@@ -214,7 +225,7 @@ class Pipeline:
             llr = modem_qam(coded, self.constellation, no, rng.child(2), self.demapper, offset=sym0)
             return payload, llr
         x = map_bits(coded, self.constellation, device=True)
-        y = awgn(x, no, rng.child(2), device=True, offset=sym0)
+        y = awgn(x, no, rng.child(2), device=True, offset=sym0, noise=self.noise)
         llr = self.demap(y, no, self.constellation, out_dtype="float32", device=True)
         return payload, llr
 
@@ -244,7 +255,7 @@ class Pipeline:
         pinned host memory on a side stream while the next chunk computes.
         """
         torch = L.torch()
-        if batch_size <= chunk:
+        if batch_size <= chunk or self.noise == "numpy":  # the numpy stream is drawn per batch
             p, d = self.run_batch_device(ebno_db, batch_size, rng)
             return L.to_host(p), L.to_host(d)
         chunk = max(32, (chunk // 32) * 32)
