@@ -98,11 +98,13 @@ int ls_standard_normal(uint64_t seed, uint64_t stream_id, int64_t count, double 
 int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
                   float *y, void *stream);
 
-/* demap_app / demap_maxlog (mapping.py:110-158) without priors for QAM/PSK
- * points: y complex64 [nsym], scalar no (>0) or per-symbol `no_vec` (nullable),
- * f64 log-domain arithmetic; llr written as f32 (`llr32`) or f64 (`llr64`),
- * whichever is non-null, m values per symbol. */
-int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec,
+/* demap_app / demap_maxlog (mapping.py:110-158) for any 2^m points:
+ * y complex64 [nsym], scalar no (>0) or per-symbol `no_vec` (nullable),
+ * optional per-bit priors `prior` [nsym, m] (LLR, added to the logits of the
+ * points whose bit is 1, mapping.py:123-131; nullable), f64 log-domain
+ * arithmetic; llr written as f32 (`llr32`) or f64 (`llr64`), whichever is
+ * non-null, m values per symbol. */
+int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
              const double *points64, int m, int mode, float *llr32, double *llr64, void *stream);
 
 /* Same as ls_demap for Gray QAM (mapping.py:33-48), using the product
@@ -110,8 +112,8 @@ int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec,
  * own axis (equal to the 2^m-point formula to ~1e-12).
  * amp[l] / lab[l] (host, 2^(m/2) entries): amplitude and axis label of level l. */
 int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec,
-                 const double *amp, const int32_t *lab, int m, int mode, float *llr32,
-                 double *llr64, void *stream);
+                 const double *prior, const double *amp, const int32_t *lab, int m, int mode,
+                 float *llr32, double *llr64, void *stream);
 
 /* Fused map_bits -> awgn -> demap_app|maxlog for Gray QAM (sweep.py:352-356
  * in one pass): coded bits [nsym*m] -> f32 LLRs [nsym*m].  The noisy symbols

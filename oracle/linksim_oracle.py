@@ -228,8 +228,8 @@ def _lse(a, axis=-1):
     return np.squeeze(shift + np.log1p(s), axis=axis)
 
 
-def demap(y, no, points, m, mode="app"):
-    """mapping.py:110-143 without priors: LLR ln(p1/p0), f64."""
+def demap(y, no, points, m, mode="app", prior=None):
+    """mapping.py:110-143: LLR ln(p1/p0), f64, optional bit priors."""
     y = np.asarray(y)
     no = np.asarray(no, np.float64)
     if np.any(no <= 0):
@@ -237,6 +237,11 @@ def demap(y, no, points, m, mode="app"):
     d2 = np.abs(y[..., None] - points) ** 2
     logits = -d2 / np.broadcast_to(no, y.shape)[..., None]
     lab = (np.arange(1 << m)[:, None] >> np.arange(m - 1, -1, -1)) & 1  # [P, m]
+    if prior is not None:  # logit of point p += sum of the priors of its 1-bits
+        prior = np.asarray(prior, np.float64)
+        if prior.shape != (m,):
+            prior = prior.reshape(*y.shape, m)
+        logits = logits + prior @ lab.T.astype(np.float64)
     out = np.empty(y.shape + (m,), np.float64)
     for j in range(m):
         one, zero = logits[..., lab[:, j] == 1], logits[..., lab[:, j] == 0]

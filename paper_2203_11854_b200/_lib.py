@@ -36,8 +36,8 @@ _SIGS = {
     "ls_binary_source": [_u64, _u64, _i64, _vp, _vp],
     "ls_map_bits": [_vp, _i64, _int, _vp, _vp, _vp],
     "ls_awgn": [_vp, _i64, _dbl, _u64, _u64, _vp, _vp],
-    "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _int, _int, _vp, _vp, _vp],
-    "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_modem_qam": [_vp, _i64, _int, _vp, _vp, _vp, _dbl, _u64, _u64, _int, _vp, _vp],
     "ls_binary_source_at": [_u64, _u64, _i64, _i64, _vp, _vp],
     "ls_standard_normal": [_u64, _u64, _i64, _vp, _vp],

@@ -185,8 +185,9 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
 // LSE(bit_j=0) with scipy's max + log1p(sum of the others), or max - max.
 template <int MAXP>
 __global__ void k_demap(const float2 *__restrict__ y, int64_t nsym, double no,
-                        const double *__restrict__ no_vec, const double2 *__restrict__ pts, int m,
-                        int mode, float *__restrict__ llr32, double *__restrict__ llr64) {
+                        const double *__restrict__ no_vec, const double *__restrict__ prior,
+                        const double2 *__restrict__ pts, int m, int mode, float *__restrict__ llr32,
+                        double *__restrict__ llr64) {
   const int P = 1 << m;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -198,6 +199,12 @@ __global__ void k_demap(const float2 *__restrict__ y, int64_t nsym, double no,
       double dr = yr - pts[p].x, di = yi - pts[p].y;
       double h = hypot(dr, di);
       lg[p] = -(h * h) / nos;
+      if (prior) {  // + bits(p) . prior (mapping.py:123-131)
+        double pr = 0.0;
+        for (int j = 0; j < m; ++j)
+          if ((p >> (m - 1 - j)) & 1) pr += prior[s * m + j];
+        lg[p] += pr;
+      }
     }
     for (int j = 0; j < m; ++j) {
       const int sh = m - 1 - j;
@@ -243,8 +250,9 @@ struct QamAxes {
 
 template <int HALF>
 __global__ void k_demap_qam(const float2 *__restrict__ y, int64_t nsym, double no,
-                            const double *__restrict__ no_vec, const QamAxes A, int mode,
-                            float *__restrict__ llr32, double *__restrict__ llr64) {
+                            const double *__restrict__ no_vec, const double *__restrict__ prior,
+                            const QamAxes A, int mode, float *__restrict__ llr32,
+                            double *__restrict__ llr64) {
   constexpr int L = 1 << HALF, M = 2 * HALF;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -259,6 +267,13 @@ __global__ void k_demap_qam(const float2 *__restrict__ y, int64_t nsym, double n
       for (int l = 0; l < L; ++l) {
         const double d = yv - A.amp[l];
         lg[l] = -(d * d) * inv;
+        if (prior) {  // the bit priors factor per axis too: bits 2t + ax of the label
+          double pr = 0.0;
+#pragma unroll
+          for (int t = 0; t < HALF; ++t)
+            if ((A.lab[l] >> (HALF - 1 - t)) & 1) pr += prior[s * M + 2 * t + ax];
+          lg[l] += pr;
+        }
       }
 #pragma unroll
       for (int t = 0; t < HALF; ++t) {
@@ -655,8 +670,8 @@ int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t st
   return ls_awgn_at(x, 0, count, no, seed, stream_id, y, stream);
 }
 
-int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *points64,
-             int m, int mode, float *llr32, double *llr64, void *stream) {
+int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+             const double *points64, int m, int mode, float *llr32, double *llr64, void *stream) {
   if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
   if (m < 1 || m > 8) return fail(LS_EINVAL, "demap: num_bits_per_symbol must be in [1, 8]");
   if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
@@ -665,17 +680,18 @@ int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, cons
   const double2 *pp = reinterpret_cast<const double2 *>(points64);
   cudaStream_t s = as_stream(stream);
   if (m <= 4)
-    k_demap<16><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+    k_demap<16><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, prior, pp, m, mode, llr32, llr64);
   else if (m <= 6)
-    k_demap<64><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+    k_demap<64><<<grid_for(nsym, 128), 128, 0, s>>>(yy, nsym, no, no_vec, prior, pp, m, mode, llr32, llr64);
   else
-    k_demap<256><<<grid_for(nsym, 64), 64, 0, s>>>(yy, nsym, no, no_vec, pp, m, mode, llr32, llr64);
+    k_demap<256><<<grid_for(nsym, 64), 64, 0, s>>>(yy, nsym, no, no_vec, prior, pp, m, mode, llr32, llr64);
   LS_CHECK_LAUNCH("ls_demap");
   return LS_OK;
 }
 
-int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, const double *amp,
-                 const int32_t *lab, int m, int mode, float *llr32, double *llr64, void *stream) {
+int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+                 const double *amp, const int32_t *lab, int m, int mode, float *llr32, double *llr64,
+                 void *stream) {
   if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
   if (m < 2 || m > 8 || (m % 2)) return fail(LS_EINVAL, "demap_qam: bits per symbol must be 2, 4, 6 or 8");
   if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
@@ -691,10 +707,10 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, 
   cudaStream_t s = as_stream(stream);
   const unsigned g = grid_for(nsym, 256);
   switch (m) {
-    case 2: k_demap_qam<1><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
-    case 4: k_demap_qam<2><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
-    case 6: k_demap_qam<3><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
-    default: k_demap_qam<4><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, mode, llr32, llr64); break;
+    case 2: k_demap_qam<1><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
+    case 4: k_demap_qam<2><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
+    case 6: k_demap_qam<3><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
+    default: k_demap_qam<4><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
   }
   LS_CHECK_LAUNCH("ls_demap_qam");
   return LS_OK;

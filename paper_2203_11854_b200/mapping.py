@@ -138,11 +138,19 @@ def map_bits(bits, constellation: Constellation, device: bool = False):
 
 
 def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str, device: bool):
-    if prior is not None:
-        raise NotImplementedError("demapper priors are not on the B200 path yet (SURVEY.md 8f #4)")
     was_np = not L.is_tensor(y)
     ty = L.to_device(y, "complex64")
     m = constellation.num_bits_per_symbol
+    tp = None
+    if prior is not None:
+        # flat prior [m] or one per bit position, broadcastable to [..., S, m]
+        # (mapping.py:123-131), laid out per symbol for the kernels
+        tp = L.to_device(prior, "float64")
+        if tuple(tp.shape) == (m,):
+            tp = tp.expand(tuple(ty.shape) + (m,))
+        else:
+            tp = tp.reshape(tuple(ty.shape) + (m,))
+        tp = tp.contiguous()
     no_arr = np.asarray(no, dtype=np.float64) if not L.is_tensor(no) else None
     no_vec = None
     if no_arr is not None and no_arr.ndim == 0:
@@ -160,10 +168,11 @@ def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str
     axes = constellation.qam_axes()
     if axes is not None:
         amp, lab = axes
-        L.call("ls_demap_qam", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), amp.ctypes.data, lab.ctypes.data,
-               m, mode, None if is64 else L.ptr(out), L.ptr(out) if is64 else None, L.stream_ptr())
+        L.call("ls_demap_qam", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), L.ptr(tp), amp.ctypes.data,
+               lab.ctypes.data, m, mode, None if is64 else L.ptr(out), L.ptr(out) if is64 else None,
+               L.stream_ptr())
         return L.to_host(out) if (was_np and not device) else out
-    L.call("ls_demap", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec),
+    L.call("ls_demap", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), L.ptr(tp),
            L.ptr(constellation.device_points("float64")), m, mode,
            None if is64 else L.ptr(out), L.ptr(out) if is64 else None, L.stream_ptr())
     return L.to_host(out) if (was_np and not device) else out

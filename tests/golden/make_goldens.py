@@ -155,6 +155,19 @@ def demap_fixture(core, mapping):
         bits = g.integers(0, 2, size=(2, 24 * m // 2), dtype=np.uint8)
         out[f"mbits{m}"] = bits
         out[f"mapped{m}"] = mapping.map_bits(bits, const)
+        # priors (mapping.py:123-131): flat [m] and per bit [..., S, m]
+        flat = g.normal(size=m)
+        full = g.normal(size=(3, 64 * m))
+        out[f"prior_flat{m}"] = flat
+        out[f"prior_full{m}"] = full
+        out[f"app_pf{m}"] = mapping.demap_app(y, 0.5, const, prior=flat)
+        out[f"app_pp{m}"] = mapping.demap_app(y, 0.5, const, prior=full)
+        out[f"maxlog_pp{m}"] = mapping.demap_maxlog(y, 0.5, const, prior=full)
+    psk = mapping.Constellation("psk", 3)
+    yp = (g.normal(size=(2, 40)) + 1j * g.normal(size=(2, 40))).astype(np.complex64)
+    out["psk_points"] = psk.points
+    out["psk_y"] = yp
+    out["psk_app"] = mapping.demap_app(yp, 0.3, psk)
     return out
 
 

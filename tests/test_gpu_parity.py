@@ -95,6 +95,20 @@ def test_map_and_demap(golden, m):
         assert np.allclose(ml, d[f"maxlog{m}_{no}"], rtol=1e-9, atol=1e-9)
 
 
+@pytest.mark.parametrize("m", [2, 4, 6])
+def test_demap_priors_and_psk(golden, m):
+    d = golden("demap")
+    const = lb.Constellation("qam", m)
+    tol = dict(rtol=1e-9, atol=1e-9)
+    assert np.allclose(lb.demap_app(d[f"y{m}"], 0.5, const, prior=d[f"prior_flat{m}"]), d[f"app_pf{m}"], **tol)
+    assert np.allclose(lb.demap_app(d[f"y{m}"], 0.5, const, prior=d[f"prior_full{m}"]), d[f"app_pp{m}"], **tol)
+    assert np.allclose(lb.demap_maxlog(d[f"y{m}"], 0.5, const, prior=d[f"prior_full{m}"]), d[f"maxlog_pp{m}"],
+                       **tol)
+    psk = lb.Constellation("psk", 3)
+    assert np.array_equal(psk.points, d["psk_points"]) and psk.qam_axes() is None
+    assert np.allclose(lb.demap_app(d["psk_y"], 0.3, psk), d["psk_app"], **tol)
+
+
 def test_demap_per_symbol_noise_and_errors():
     const = lb.Constellation("qam", 4)
     g = np.random.default_rng(3)

@@ -70,6 +70,18 @@ def test_mapping_and_demapping(golden, m):
         assert np.allclose(ml, d[f"maxlog{m}_{no}"], rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("m", [2, 4, 6])
+def test_demapping_with_priors_and_psk(golden, m):
+    d = golden("demap")
+    pts = O.qam_points(m)
+    tol = dict(rtol=1e-12, atol=1e-12)
+    assert np.allclose(O.demap(d[f"y{m}"], 0.5, pts, m, "app", d[f"prior_flat{m}"]), d[f"app_pf{m}"], **tol)
+    assert np.allclose(O.demap(d[f"y{m}"], 0.5, pts, m, "app", d[f"prior_full{m}"]), d[f"app_pp{m}"], **tol)
+    assert np.allclose(O.demap(d[f"y{m}"], 0.5, pts, m, "maxlog", d[f"prior_full{m}"]), d[f"maxlog_pp{m}"],
+                       **tol)
+    assert np.allclose(O.demap(d["psk_y"], 0.3, d["psk_points"], 3, "app"), d["psk_app"], **tol)
+
+
 @pytest.mark.parametrize("variant", ["sum-product", "min-sum", "scaled-min-sum"])
 @pytest.mark.parametrize("es", [0, 1])
 @pytest.mark.parametrize("dt", ["64", "32"])
