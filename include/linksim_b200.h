@@ -168,6 +168,7 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
 #define LS_QC_PRUNE 1
 #define LS_QC_GENERIC 2
 #define LS_QC_FP16 4 /* packed fp16x2 kernel: two codewords per 32-bit lane */
+#define LS_QC_SP 8   /* ls_qc_has_kernel only: ask for the sum-product kernel */
 int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
                  double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,
                  int32_t *iters_used, const uint8_t *ref_bits, unsigned long long *counts,

@@ -219,6 +219,7 @@ namespace lsb {
 LSB_QC_INSTANCES(LSB_QC_DECL)
 #define LSB_QC_PREC_f32 0
 #define LSB_QC_PREC_h2 1
+#define LSB_QC_PREC_sp 2
 #define LSB_QC_ENTRY(bg, z, r, sp, pr) {bg, z, r, LSB_QC_PREC_##pr, &qc2_##pr##_##bg##_##z##_##r},
 static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
 
@@ -235,10 +236,15 @@ int live_rows(const QcParams &P) {
 
 extern "C" int ls_qc_live_rows(const ls_code *code) { return code ? live_rows(code->p) : -1; }
 
+// kernel kind: 0 fp32 min-sum, 1 fp16x2 min-sum, 2 sum-product
+static int qc_kind(int variant, int flags) {
+  return variant == LS_SUM_PRODUCT ? 2 : ((flags & LS_QC_FP16) ? 1 : 0);
+}
+
 extern "C" int ls_qc_has_kernel(const ls_code *code, int flags) {
   if (!code) return 0;
   const int R = (flags & LS_QC_PRUNE) ? live_rows(code->p) : code->p.mb;
-  const int prec = (flags & LS_QC_FP16) ? 1 : 0;
+  const int prec = (flags & LS_QC_SP) ? 2 : qc_kind(LS_MIN_SUM, flags);
   for (const QcKernelEntry &k : kQcKernels)
     if (k.bg == code->p.bg && k.z == code->p.z && k.r == R && k.prec == prec) return 1;
   return 0;
@@ -251,23 +257,25 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   if (!code) return fail(LS_EINVAL, "ls_qc_decode: null code");
   if (variant < 0 || variant > 2) return fail(LS_EINVAL, "unknown BP variant");
   if (num_iter < 1) return fail(LS_EINVAL, "num_iter must be >= 1");
-  if (variant == LS_SUM_PRODUCT) return fail(LS_EINVAL, "ls_qc_decode: sum-product fast mode not built yet");
   if (batch <= 0) return LS_OK;
   const QcParams &P = code->p;
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
-  if ((flags & LS_QC_FP16) && (flags & LS_QC_GENERIC))
-    return fail(LS_EINVAL, "ls_qc_decode: the fp16x2 decoder has no runtime-Z kernel");
+  const int prec = qc_kind(variant, flags);
+  if (prec && (flags & LS_QC_GENERIC))
+    return fail(LS_EINVAL, "ls_qc_decode: the fp16x2 and sum-product decoders have no runtime-Z kernel");
   if (!(flags & LS_QC_GENERIC)) {
     const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
-    const int prec = (flags & LS_QC_FP16) ? 1 : 0;
     for (const QcKernelEntry &k : kQcKernels) {
       if (k.bg == P.bg && k.z == P.z && k.r == R && k.prec == prec) {
         QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
         return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
       }
     }
-    if (prec) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
+    if (prec == 1) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
+    if (prec == 2)
+      return fail(LS_EINVAL, "ls_qc_decode: no sum-product fast decoder instance for this (BG, Z, rows); "
+                             "use the exact decoder");
   }
   QcFastParams FP;
   FP.z = P.z; FP.k = P.k; FP.n = P.n; FP.k_full = P.k_full; FP.n_full = P.n_full; FP.l1 = P.l1;

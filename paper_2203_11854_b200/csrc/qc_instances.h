@@ -1,10 +1,12 @@
 // Specialised fast-decoder instances compiled in: (base graph, Z, processed
-// rows, threads per lane, precision).  Each becomes build/gen/qc_<...>.cu.
-// Codes matching none of them use the runtime-Z fp32 kernel in bp_fast.cu.
+// rows, threads per lane, kind).  Each becomes build/gen/qc_<...>.cu.
+// Min-sum codes matching none of them use the runtime-Z fp32 kernel in
+// bp_fast.cu; sum-product fast mode exists only for these instances.
 //   1,384,24 / 1,384,46 : config 2 (k=8448 n=16896), dead rows pruned / all
 //   1,192,{24,45,46}    : configs 3 and 4 (k=4096, n=8192 / 12288)
 //   2,26,{12,42}        : config 1 (k=256 n=512)
-// precision f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh)
+// kind f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh);
+// sp: k_qc_sp, sum-product (bp_fast_sp.cuh)
 #pragma once
 #define LSB_QC_INSTANCES(X) \
   X(1, 384, 24, 2, f32)     \
@@ -20,4 +22,10 @@
   X(1, 192, 45, 2, h2)      \
   X(1, 192, 46, 2, h2)      \
   X(2, 26, 12, 1, h2)       \
-  X(2, 26, 42, 1, h2)
+  X(2, 26, 42, 1, h2)       \
+  X(1, 384, 24, 2, sp)      \
+  X(1, 192, 24, 2, sp)      \
+  X(1, 192, 45, 2, sp)      \
+  X(1, 192, 46, 2, sp)      \
+  X(2, 26, 12, 1, sp)       \
+  X(2, 26, 42, 1, sp)

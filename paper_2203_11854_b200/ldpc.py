@@ -249,12 +249,16 @@ def _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, prec
     return out.numpy() if not L.is_tensor(llr) else out
 
 
-LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16 = 1, 2, 4
+LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP = 1, 2, 4, 8
 
 
-def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True) -> bool:
-    """Whether a compile-time specialised fast decoder exists for this code."""
+def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
+                  variant: str = "min-sum") -> bool:
+    """Whether a compile-time specialised fast decoder exists for this code
+    (the sum-product fast decoder exists only as such instances)."""
     flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
+    if variant == "sum-product":
+        flags |= LS_QC_SP
     return bool(L.lib().ls_qc_has_kernel(code.handle, flags))
 
 

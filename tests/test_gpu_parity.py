@@ -302,6 +302,35 @@ def test_fast_fp16x2_decoder(k, n, m, ebno, variant, es):
     assert (clean["iters"].cpu().numpy() <= 2).all()
 
 
+@pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 2.5), (8448, 16896, 4, 4.6), (4096, 12288, 6, 5.5),
+                                        (4096, 8192, 2, 1.8)])
+@pytest.mark.parametrize("es", [True, False])
+def test_fast_sum_product_decoder(k, n, m, ebno, es):
+    """Sum-product fast mode (per-edge fp16 messages on chip) against the
+    reference's sum-product: converged blocks identical, block errors close."""
+    B = 48 if k < 5000 else 12
+    bits, llr = _oracle_llrs(k, n, m, ebno, B, 13)
+    code = lb.LdpcCode5G(k, n)
+    assert lb.ldpc.qc_has_kernel(code, variant="sum-product")
+    res = lb.qc_decode(llr, code, 20, "sum-product", early_stop=es, ref_bits=bits, want_iters=True)
+    hard = res["hard"].cpu().numpy()
+    ref_hard, _, it_o = O.decode(llr, O.code(k, n), 20, "sum-product", 0.75, True)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    ok_fast = (hard == bits).all(axis=1)
+    conv = (it_o < 20) & ok_ref
+    assert conv.sum() >= B // 4
+    assert np.array_equal(hard[conv], ref_hard[conv])
+    assert (ok_ref != ok_fast).sum() <= max(1, B // 12)
+    cnt = res["counts"].cpu().numpy()
+    assert cnt[0] == int((hard != bits).sum()) and cnt[1] == int((~ok_fast).sum())
+    it = res["iters"].cpu().numpy()
+    if es:
+        # sum-product converges in about as many iterations as the reference
+        assert abs(it[conv].mean() - it_o[conv].mean()) <= 1.5
+    else:
+        assert (it == 20).all()
+
+
 def test_fast_decoder_noiseless_round_trip_and_early_stop():
     for k, n in [(500, 1000), (100, 300), (8448, 16896), (4096, 12288), (256, 1536)]:
         code = lb.LdpcCode5G(k, n)
