@@ -34,11 +34,15 @@ struct QcShapeSP {
 };
 
 // phi(x) = -log(tanh(x / 2)) on the reference's clip range [1e-12, 40]
+// (3 MUFU: ex2, rcp, lg2; branch-free).  phi(x) = ln((1 + u) / (1 - u)) with
+// u = e^-x; for small x the denominator 1 - u comes from its Taylor series
+// (no cancellation).
 __device__ __forceinline__ float sp_phi(float x) {
   x = fminf(fmaxf(x, 1e-12f), 40.0f);
-  if (x < 0.0625f) return __logf(2.0f / x) + x * x * (1.0f / 12.0f);  // series, avoids 1 - e^-x
-  const float e = __expf(-x);
-  return __logf(__fdividef(1.0f + e, 1.0f - e));
+  const float u = __expf(-x);
+  const float series = x * fmaf(x, fmaf(x, fmaf(x, -1.0f / 24.0f, 1.0f / 6.0f), -0.5f), 1.0f);
+  const float om = x < 0.0625f ? series : 1.0f - u;
+  return __logf(__fdividef(1.0f + u, om));
 }
 
 template <class G, int Z, int E>
