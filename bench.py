@@ -245,7 +245,11 @@ def run_b200(a, rank, world, local_rank):
             "config": dict(_workload(a), decoder_precision=pipe.precision, fused_modem=pipe.fused_modem),
             "gpu_launches": (4 if pipe.fused_modem else 6) * a.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         # DRAM bytes per launch: ncu --set full capture of k_qc_fast_h2 on 2368
+                         # codewords (184.1 MB read+write, profiles/r01/), scaled to this batch;
+                         # the messages never leave the SM, DRAM sees the LLR input only
+                         "traffic": (B * 184_096_256 / 2368) if pipe.precision == "fp16x2" else None,
                          "kernel": "k_qc_fast_h2" if pipe.precision == "fp16x2" else "k_qc_fast2",
                          "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
                          "kernel_ms_per_launch": per_launch_ms,
