@@ -5,6 +5,8 @@
 //   1,384,24 / 1,384,46 : config 2 (k=8448 n=16896), dead rows pruned / all
 //   1,192,{24,45,46}    : configs 3 and 4 (k=4096, n=8192 / 12288)
 //   2,26,{12,42}        : config 1 (k=256 n=512)
+//   1,Z,24 / 2,Z,22 for Z in 32..384 : config 5 decoder-only sweep (BG1 rate
+//                         1/2 and BG2 rate 1/3 lifted at any Z, fp16x2)
 // kind f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh);
 // sp: k_qc_sp, sum-product (bp_fast_sp.cuh)
 #pragma once
@@ -23,6 +25,16 @@
   X(1, 192, 46, 2, h2)      \
   X(2, 26, 12, 1, h2)       \
   X(2, 26, 42, 1, h2)       \
+  X(1, 32, 24, 4, h2)       \
+  X(1, 64, 24, 4, h2)       \
+  X(1, 128, 24, 4, h2)      \
+  X(1, 256, 24, 2, h2)      \
+  X(2, 32, 22, 4, h2)       \
+  X(2, 64, 22, 4, h2)       \
+  X(2, 128, 22, 4, h2)      \
+  X(2, 192, 22, 4, h2)      \
+  X(2, 256, 22, 2, h2)      \
+  X(2, 384, 22, 2, h2)      \
   X(1, 384, 24, 2, sp)      \
   X(1, 192, 24, 2, sp)      \
   X(1, 192, 45, 2, sp)      \

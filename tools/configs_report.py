@@ -24,7 +24,7 @@ import torch  # noqa: E402
 import paper_2203_11854_b200 as lb  # noqa: E402
 
 
-def config3(quick):
+def config3(quick, outdir):
     pts = [0.0, 0.5, 1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0, 4.5, 5.0, 5.5, 6.0]
     res = {}
     for variant in ("min-sum", "sum-product"):
@@ -40,7 +40,7 @@ def config3(quick):
         torch.cuda.synchronize()
         el = time.perf_counter() - t
         csv = lb.format_csv(r)
-        with open(os.path.join(ROOT, "profiles", "r01", f"sweep_c3_{variant}.csv"), "w") as f:
+        with open(os.path.join(outdir, f"sweep_c3_{variant}.csv"), "w") as f:
             f.write(csv)
         res[variant] = {"elapsed_s": el, "points": [
             {"ebno_db": p.ebno_db, "bits": p.bits, "bit_errors": p.bit_errors, "ber": p.ber,
@@ -49,6 +49,9 @@ def config3(quick):
             "decoded_bits": sum(p.bits for p in r.points),
             "throughput_gbit_s": sum(p.bits for p in r.points) / el / 1e9}
     return res
+
+
+EB4 = 8.0  # 64-QAM rate 1/3 on the synthetic BG1 sits in its waterfall near 7-8 dB
 
 
 def config4(quick):
@@ -60,22 +63,22 @@ def config4(quick):
             "code": {"family": "ldpc5g", "k": k, "n": n,
                      "decoder": {"variant": "min-sum", "mode": "fast", "num_iter": 20, "early_stop": False}},
             "modulation": {"kind": "qam", "bits_per_symbol": m, "demapper": demapper},
-            "sweep": {"ebno_db": [7.0], "batch_size": B}, "seed": 7})
+            "sweep": {"ebno_db": [EB4], "batch_size": B}, "seed": 7})
         pipe = lb.Pipeline(cfg)
         counts = torch.zeros(2, dtype=torch.int64, device="cuda")
-        pipe.run_batch_counts(7.0, B, lb.RngStream(7, 1), counts)
+        pipe.run_batch_counts(EB4, B, lb.RngStream(7, 1), counts)
         torch.cuda.synchronize()
         counts.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         steps = 3
         for s in range(steps):
-            pipe.run_batch_counts(7.0, B, lb.RngStream(7, 10 + s), counts)
+            pipe.run_batch_counts(EB4, B, lb.RngStream(7, 10 + s), counts)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         c = counts.cpu().tolist()
-        out[demapper] = {"batch": B, "ebno_db": 7.0, "ms_per_batch": ms, "gbit_s": B * k / ms / 1e6,
+        out[demapper] = {"batch": B, "ebno_db": EB4, "ms_per_batch": ms, "gbit_s": B * k / ms / 1e6,
                          "ber": c[0] / (steps * B * k), "bler": c[1] / (steps * B),
                          "decoder_precision": pipe.precision, "fused_modem": pipe.fused_modem}
     return out
@@ -83,7 +86,7 @@ def config4(quick):
 
 def config5(quick):
     iters = [5, 10, 20, 50]
-    zs = [32, 64, 96, 128, 192, 256, 384] if not quick else [96, 384]
+    zs = [32, 64, 96, 128, 192, 256, 384] if not quick else [96, 384]  # 96: runtime-Z kernel
     rows = []
     for bg in (1, 2):
         kb = 22 if bg == 1 else 10
@@ -112,7 +115,9 @@ def config5(quick):
                                  "kernel": ("specialised " + prec) if lb.ldpc.qc_has_kernel(code, prec) or
                                  variant == "sum-product" else "runtime-Z fp32",
                                  "batch": B, "ms": ms, "info_gbit_s": B * k / ms / 1e6,
-                                 "edge_updates_per_s": B * it * code.pcm.num_edges / (ms / 1e3)})
+                                 "live_rows": int(lb._lib.lib().ls_qc_live_rows(code.handle)),
+                                 "mother_graph_edge_updates_per_s":
+                                     B * it * code.pcm.num_edges / (ms / 1e3)})
     return rows
 
 
@@ -125,7 +130,7 @@ def main():
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     rep = {"device": torch.cuda.get_device_name(0)}
     if "3" in a.only:
-        rep["config3_sweep"] = config3(a.quick)
+        rep["config3_sweep"] = config3(a.quick, os.path.dirname(os.path.abspath(a.out)))
     if "4" in a.only:
         rep["config4_64qam"] = config4(a.quick)
     if "5" in a.only:
