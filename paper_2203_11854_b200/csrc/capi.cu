@@ -414,7 +414,7 @@ template <class G>
 __global__ void __launch_bounds__(128) k_encode_packed(QcParams P, const uint8_t *__restrict__ bits,
                                                        uint8_t *__restrict__ tx, uint8_t *__restrict__ full) {
   constexpr int KB = G::KB, MB = G::MB;
-  __shared__ uint32_t flat[(KB * 384) / 32 + 2];  // systematic bits, flat
+  __shared__ uint32_t flat[(G::NB * 384) / 32 + 2];  // systematic bits, then the whole codeword
   __shared__ uint32_t xd[KB][kEncD];               // doubled systematic columns
   __shared__ uint32_t syn[MB][kEncW];              // syndromes, then extension parities
   __shared__ uint32_t core[4][kEncW + 1];
@@ -500,24 +500,49 @@ __global__ void __launch_bounds__(128) k_encode_packed(QcParams P, const uint8_t
     syn[r][w] = (w == W - 1) ? (acc & lastmask) : acc;
   }
   __syncthreads();
-  // 6. unpack: mother codeword and the rate-matched gather (ldpc.py:351)
-  for (int c = 0; c < G::NB; ++c) {
-    for (int i = t; i < Z; i += NT) {
-      const int v = c * Z + i;
-      uint32_t word;
-      if (c < KB) {
-        const int pos = v;
-        word = bits_at(flat, pos) & 1u;
-      } else if (c < KB + 4) {
-        word = (core[c - KB][i >> 5] >> (i & 31)) & 1u;
+  // 6. the mother codeword as one flat bit array (systematic bits are already
+  //    in place in `flat`; append the parity columns)
+  //    (each word is read and written by one thread only)
+  uint32_t *cwf = flat;
+  const int nwords = (P.n_full + 31) >> 5, w0 = P.k_full >> 5;
+  for (int w = w0 + t; w < nwords + 1; w += NT) {
+    uint32_t out = 0;
+    int filled = 0;
+    if (w == w0 && (P.k_full & 31)) {  // shared with the systematic tail
+      filled = P.k_full & 31;
+      out = flat[w] & ((1u << filled) - 1u);
+    }
+    while (filled < 32) {
+      const int v = 32 * w + filled;
+      if (v >= P.n_full) break;
+      const int c = v / Z, i = v - c * Z;
+      const int take = min(32 - filled, Z - i);
+      const uint32_t *src = c < KB + 4 ? core[c - KB] : syn[c - KB];
+      uint32_t bitsv = bits_at(src, i);
+      if (take < 32) bitsv &= (1u << take) - 1u;
+      out |= bitsv << filled;
+      filled += take;
+    }
+    cwf[w] = out;
+  }
+  __syncthreads();
+  // 7. outputs (ldpc.py:351): 16 rate-matched bits per thread, as one 16-byte store
+  if (full) {
+    for (int v = t; v < P.n_full; v += NT) full[b * (int64_t)P.n_full + v] = (uint8_t)(bits_at(cwf, v) & 1u);
+  }
+  if (tx) {
+    uint8_t *o = tx + b * (int64_t)P.n;
+    const bool al = ((reinterpret_cast<uintptr_t>(o) & 15) == 0);
+    for (int j0 = 16 * t; j0 < P.n; j0 += 16 * NT) {
+      const int v0 = mother_of(P, j0);
+      if (al && j0 + 16 <= P.n && mother_of(P, j0 + 15) == v0 + 15) {
+        const uint32_t b16 = bits_at(cwf, v0);
+        uint32_t wv[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) wv[g] = (((b16 >> (4 * g)) & 15u) * 0x00204081u) & 0x01010101u;
+        *reinterpret_cast<uint4 *>(o + j0) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       } else {
-        word = (syn[c - KB][i >> 5] >> (i & 31)) & 1u;
-      }
-      const uint8_t bit = (uint8_t)word;
-      if (full) full[b * (int64_t)P.n_full + v] = bit;
-      if (tx && v >= 2 * Z && !(v >= P.k && v < P.k_full)) {
-        const int pos = v < P.k ? v - 2 * Z : P.l1 + (v - P.k_full);
-        for (int j = pos; j < P.n; j += P.buflen) tx[b * (int64_t)P.n + j] = bit;
+        for (int j = j0; j < min(j0 + 16, P.n); ++j) o[j] = (uint8_t)(bits_at(cwf, mother_of(P, j)) & 1u);
       }
     }
   }

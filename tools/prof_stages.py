@@ -14,6 +14,7 @@ p.add_argument("--k", type=int, default=8448)
 p.add_argument("--n", type=int, default=16896)
 p.add_argument("--m", type=int, default=4)
 p.add_argument("--ebno", type=float, default=6.0)
+p.add_argument("--noise", default="philox", choices=["philox", "numpy"])
 a = p.parse_args()
 code = lb.LdpcCode5G(a.k, a.n)
 const = lb.Constellation("qam", a.m)
@@ -30,7 +31,7 @@ def run(timed):
     ev[2].record()
     x = lb.map_bits(tx, const, device=True)
     ev[3].record()
-    y = lb.awgn(x, no, rng.child(2), device=True)
+    y = lb.awgn(x, no, rng.child(2), device=True, noise=a.noise)
     ev[4].record()
     llr = lb.demap_app(y, no, const, out_dtype="float32", device=True)
     ev[5].record()
