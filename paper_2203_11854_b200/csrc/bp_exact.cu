@@ -224,19 +224,7 @@ static int run_exact(const ls_graph *g, const T *llr, int64_t B, int num_iter, i
   uint8_t *flags = nullptr;
   int32_t *iters = nullptr;
   cudaError_t e;
-  {
-    // keep the stream-ordered pool's memory between calls (the workspace is
-    // [E, B] f64, ~1 GB for 1024 BG1 Z=384 codewords)
-    static std::once_flag once;
-    std::call_once(once, [] {
-      int dev = 0;
-      cudaMemPool_t pool;
-      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-    });
-  }
+  retain_pool_memory();  // the workspace is [E, B] f64, ~1 GB for 1024 BG1 Z=384 codewords
 #define LS_TRY(x)                                \
   do {                                           \
     e = (x);                                     \

@@ -24,6 +24,10 @@ int cuda_status(cudaError_t e, const char *where);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// keep the stream-ordered allocator's memory between calls (workspaces of the
+// exact decoder and of the numpy-normal replica are GB-sized)
+void retain_pool_memory();
+
 inline unsigned grid_for(int64_t n, int block, int64_t cap = 148LL * 64) {
   int64_t g = (n + block - 1) / block;
   if (g > cap) g = cap;

@@ -208,25 +208,74 @@ __global__ void k_zig_assign(const uint32_t *__restrict__ trans, int64_t nseg, i
   }
 }
 
-__global__ void k_zig_emit(uint64_t seed, uint64_t sid, int64_t nseg, const int *__restrict__ sentry,
-                           const int64_t *__restrict__ sbase, int64_t count, double *__restrict__ out,
-                           int *__restrict__ overflow) {
+// One block of 256 threads per segment; thread t owns the 4 words of Philox
+// block t (positions 4t..4t+3), so each word is generated once: fast-path
+// draws are evaluated from the registers, only the rare multi-word draws
+// re-read the stream.
+__global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, int64_t nseg,
+                                                  const int *__restrict__ sentry, const int64_t *__restrict__ sbase,
+                                                  int64_t count, double *__restrict__ out, int *__restrict__ overflow) {
   __shared__ uint16_t spos[kZSpec], slen[kZSpec];
   __shared__ int cnt_s;
+  const int t = threadIdx.x;
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
     const int64_t base = sbase[s];
     if (base >= count) continue;  // uniform per block
-    const int n = zig_specials(seed, sid, s, spos, slen, &cnt_s, overflow);
+    if (t == 0) cnt_s = 0;
+    __syncthreads();
+    uint64_t w[4];
+    philox4x64_10((uint64_t)(s * (kZG / 4) + t) + 1, 0, 0, 0, sid, seed, w);
+    double val[4];
+    int len[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = (int)(w[u] & 0xff);
+      const uint64_t r = w[u] >> 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      double x = (double)rabs * ls_zig_wi[idx];
+      if (r & 0x1) x = -x;
+      len[u] = 1;
+      val[u] = x;
+      if (!(rabs < ls_zig_ki[idx])) {
+        val[u] = zig_draw(seed, sid, s * kZG + 4 * t + u, &len[u]);
+        const int k = atomicAdd(&cnt_s, 1);
+        if (k < kZSpec) {
+          spos[k] = (uint16_t)(4 * t + u);
+          slen[k] = (uint16_t)min(len[u], 65535);
+        } else {
+          *overflow = 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int n = min(cnt_s, kZSpec);
+    if (t == 0) {
+      for (int a = 1; a < n; ++a) {
+        const uint16_t p = spos[a], l = slen[a];
+        int b = a - 1;
+        while (b >= 0 && spos[b] > p) {
+          spos[b + 1] = spos[b];
+          slen[b + 1] = slen[b];
+          --b;
+        }
+        spos[b + 1] = p;
+        slen[b + 1] = l;
+      }
+    }
+    __syncthreads();
     const int e = sentry[s];
-    for (int p = threadIdx.x; p < kZG; p += blockDim.x) {
-      if (p < e) continue;
-      int cnt, cur;
-      zig_walk(spos, slen, n, e, p, &cnt, &cur);
-      if (p < cur) continue;  // consumed by an earlier multi-word draw
-      const int64_t j = base + cnt + (p - cur);
-      if (j < count) {
-        int len;
-        out[j] = zig_draw(seed, sid, s * kZG + p, &len);
+    int cnt, cur;
+    zig_walk(spos, slen, n, e, 4 * t, &cnt, &cur);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = 4 * t + u;
+      if (p >= cur) {  // a draw starts here (cur >= e always)
+        const int64_t j = base + cnt + (p - cur);
+        if (j < count) out[j] = val[u];
+        if (len[u] > 1) {  // multi-word draw: the next start is p + len
+          cnt += p - cur + 1;
+          cur = p + len[u];
+        }
       }
     }
     __syncthreads();
@@ -245,6 +294,7 @@ __global__ void k_awgn_apply(const float2 *__restrict__ x, int64_t S, double sca
 }
 
 static int normals(uint64_t seed, uint64_t sid, int64_t count, double *out, cudaStream_t s) {
+  retain_pool_memory();
   const int64_t words = (int64_t)((double)count * 1.06) + 8 * kZG;
   const int64_t nseg = (words + kZG - 1) / kZG;
   const int64_t ngroups = (nseg + kZGroup - 1) / kZGroup;
