@@ -364,11 +364,24 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
   if (batch < 0) return fail(LS_EINVAL, "ls_bp_decode: negative batch");
   if (!batch) return LS_OK;
   cudaStream_t s = as_stream(stream);
-  if (is_f64)
-    return run_exact<double>(g, (const double *)llr, batch, num_iter, variant, scale, early_stop,
-                             (double *)llr_out, hard, iters_used, s);
-  return run_exact<float>(g, (const float *)llr, batch, num_iter, variant, scale, early_stop, (float *)llr_out,
-                          hard, iters_used, s);
+  // rows are independent: bound the [E, B] f64 workspace to ~8 GB by
+  // decoding in row chunks (same results as one call)
+  const int64_t per_row = 8 * std::max<int64_t>(g->E, 1) + 16 * g->n + 16;
+  const int64_t chunk = std::max<int64_t>(32, (8LL << 30) / per_row);
+  const size_t esz = is_f64 ? 8 : 4;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int64_t nb = std::min(chunk, batch - b0);
+    const char *in = (const char *)llr + (size_t)b0 * g->n * esz;
+    char *out = llr_out ? (char *)llr_out + (size_t)b0 * g->n * esz : nullptr;
+    uint8_t *hd = hard ? hard + (size_t)b0 * g->n : nullptr;
+    int32_t *it = iters_used ? iters_used + b0 : nullptr;
+    const int rc = is_f64 ? run_exact<double>(g, (const double *)in, nb, num_iter, variant, scale, early_stop,
+                                              (double *)out, hd, it, s)
+                          : run_exact<float>(g, (const float *)in, nb, num_iter, variant, scale, early_stop,
+                                             (float *)out, hd, it, s);
+    if (rc != LS_OK) return rc;
+  }
+  return LS_OK;
 }
 
 }  // extern "C"
