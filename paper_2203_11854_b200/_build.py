@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "liblinksim_b200.so")
 SOURCES = ["capi.cu", "bp_exact.cu", "bp_fast.cu", "rng_normal.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wshadow",
          "-I", os.path.join(ROOT, "include")]
 
 

@@ -18,6 +18,8 @@
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "bp_fast_qc.cuh"
 
 namespace lsb {
@@ -53,10 +55,10 @@ struct QcShapeH2 {
   static constexpr int MINB = NT >= 384 ? 1 : (384 / NT);
 };
 
-// per-codeword outputs of half `HB` (0 = A, 1 = B) from the current posteriors
-template <int NT, int HB>
+// per-codeword outputs of half `hb` (0 = A, 1 = B) from the current posteriors
+template <int NT>
 __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *tot, int nv, int64_t cw,
-                                        const float *row, int used, uint8_t *hard_k, float *llr_out,
+                                        const float *row, int hb, int used, uint8_t *hard_k, float *llr_out,
                                         int32_t *iters_used, const uint8_t *ref, unsigned long long *counts,
                                         unsigned *red) {
   const int t = threadIdx.x;
@@ -67,7 +69,7 @@ __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *t
       float val;
       if (v < nv) {
         const uint32_t w = tot[v];
-        val = -__half2float(__ushort_as_half((unsigned short)(HB ? (w >> 16) : (w & 0xFFFFu))));
+        val = -__half2float(__ushort_as_half((unsigned short)(hb ? (w >> 16) : (w & 0xFFFFu))));
       } else {
         val = -chan_value(P, row, v);
       }
@@ -77,8 +79,8 @@ __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *t
   unsigned err = 0;
   for (int v = t; v < P.k; v += NT) {
     const uint32_t w = tot[v];
-    const unsigned short hb = (unsigned short)(HB ? (w >> 16) : (w & 0xFFFFu));
-    const uint8_t hd = (-__half2float(__ushort_as_half(hb))) > 0.0f;
+    const unsigned short hv = (unsigned short)(hb ? (w >> 16) : (w & 0xFFFFu));
+    const uint8_t hd = (-__half2float(__ushort_as_half(hv))) > 0.0f;
     if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
     if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
   }
@@ -97,6 +99,184 @@ __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *t
     }
     __syncthreads();
   }
+}
+
+// per-thread compressed check state of the thread's NR rows (registers once
+// the phase functions are inlined with compile-time row indices)
+template <int NR>
+struct H2State {
+  uint32_t M1[NR], M2[NR], IX[NR], SG[NR], SG2[NR];
+};
+
+// Check-node phase of one iteration for the calling thread's rows; returns
+// the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B).
+template <class G, int Z, int R, int SPLIT, int NR>
+__device__ __forceinline__ uint32_t h2_cn(H2State<NR> &st, const char *base, int h, bool lane, __half2 al2,
+                                         bool scaled) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  uint32_t synx = 0;
+  if (!lane) return 0;
+  sfor<0, SPLIT>([&](auto hc) {
+    constexpr int H = decltype(hc)::value;
+    if (h != H) return;
+    const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
+    sfor<0, NR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      constexpr int r = j * SPLIT + H;
+      if constexpr (r < R) {
+        constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
+        constexpr bool packed = d <= 16;
+        // ALU-pipe relief: the min1/min2 select and the argmin update are
+        // fp16 FMAs on 1.0/0.0 compare results (FMA pipe)
+        const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
+        const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
+        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u;
+        __half2 nix = u2h(0u);
+        sfor<e0, e1>([&](auto ec) {
+          constexpr int e = decltype(ec)::value;
+          constexpr int p = e - e0;
+          const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + vn_off<G, Z, e>(i4));
+          hs ^= tw;
+          const __half2 pp = u2h(h2_int<p>());
+          const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
+          uint32_t sgn;
+          if constexpr (packed) {
+            sgn = (osg << (15 - p)) & 0x80008000u;
+          } else {
+            const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+            sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+          }
+          const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
+          const uint32_t xw = h2u(x);
+          const __half2 a = __habs2(x);
+          nix = __hfma2(__hlt2(a, u2h(n1)), __hsub2(pp, nix), nix);
+          n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
+          n1 = h2u(__hmin2(u2h(n1), a));
+          if constexpr (packed) {
+            if constexpr (p == 15)
+              sg |= xw & 0x80008000u;
+            else
+              sg |= __umulhi(xw, 1u << (17 + p)) & (0x10001u << p);  // xw >> (15 - p)
+          } else {
+            sg |= ((xw >> 15) & 1u) << p;
+            sg2 |= (xw >> 31) << p;
+          }
+        });
+        constexpr uint32_t dm = (1u << d) - 1u;
+        if constexpr (packed) {
+          const uint32_t pa = __popc(sg & 0xFFFFu) & 1u, pb = __popc(sg >> 16) & 1u;
+          st.SG[j] = sg ^ (((0u - pa) & dm) | ((0u - pb) & (dm << 16)));
+        } else {
+          const uint32_t pa = __popc(sg) & 1u, pb = __popc(sg2) & 1u;
+          st.SG[j] = sg ^ ((0u - pa) & dm);
+          st.SG2[j] = sg2 ^ ((0u - pb) & dm);
+        }
+        if (scaled) {
+          n1 = h2u(__hmul2(u2h(n1), al2));
+          n2 = h2u(__hmul2(u2h(n2), al2));
+        }
+        // state keeps min1 and the fp16 difference min2 - min1; the argmin
+        // edge is reconstructed as min1 + diff (within 1 ulp of min2)
+        st.M1[j] = n1;
+        st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
+        st.IX[j] = h2u(nix);
+        synx |= hs;
+      }
+    });
+  });
+  return synx;
+}
+
+// Variable-node phase: posteriors = clip(chan + sum of the new messages).
+// `chan_word(v)` supplies the channel half2 of VN v when it is not cached.
+template <class G, int Z, int R, int SPLIT, int NR, class ChanFn>
+__device__ __forceinline__ void h2_vn(const H2State<NR> &st, uint32_t *tot, const uint32_t *chn, char *base, int h,
+                                      bool lane, int t, ChanFn chan_word) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  if constexpr (S::CHN_SMEM && S::NV % 4 == 0) {
+    // 128-bit shared accesses: 4 posteriors (8 messages) per instruction
+    uint4 *t4 = reinterpret_cast<uint4 *>(tot);
+    const uint4 *c4 = reinterpret_cast<const uint4 *>(chn);
+    for (int v = t; v < S::NV / 4; v += S::NT) {
+      t4[v] = c4[v];
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) t4[q * (S::NV / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  } else {
+    for (int v = t; v < S::NV; v += S::NT) {
+      uint32_t ch;
+      if constexpr (S::CHN_SMEM) {
+        ch = chn[v];
+      } else {
+        ch = chan_word(v);
+      }
+      tot[v] = ch;
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) tot[q * S::NV + v] = 0u;
+    }
+  }
+  __syncthreads();
+  sfor<0, NR>([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    if (lane) {
+      sfor<0, SPLIT>([&](auto hc) {
+        constexpr int H = decltype(hc)::value;
+        constexpr int r = j * SPLIT + H;
+        if constexpr (r < R) {
+          if (h != H) return;
+          constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
+          constexpr bool packed = d <= 16;
+          const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
+          char *const arr = base + 4u * H * S::NV;
+          const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
+          const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
+          sfor<e0, e1>([&](auto ec) {
+            constexpr int e = decltype(ec)::value;
+            constexpr int p = e - e0;
+            uint32_t *tp = reinterpret_cast<uint32_t *>(arr + vn_off<G, Z, e>(i4));
+            const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
+            uint32_t sgn;
+            if constexpr (packed) {
+              sgn = (osg << (15 - p)) & 0x80008000u;
+            } else {
+              const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+              sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+            }
+            *tp = h2u(__hadd2(u2h(*tp), u2h(mag | sgn)));
+          });
+        }
+      });
+    }
+    __syncthreads();
+  });
+  const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
+  if constexpr (S::NV % 4 == 0) {
+    uint4 *t4 = reinterpret_cast<uint4 *>(tot);
+    for (int v = t; v < S::NV / 4; v += S::NT) {
+      uint4 a = t4[v];
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) {
+        const uint4 o = t4[q * (S::NV / 4) + v];
+        a.x = h2u(__hadd2(u2h(a.x), u2h(o.x)));
+        a.y = h2u(__hadd2(u2h(a.y), u2h(o.y)));
+        a.z = h2u(__hadd2(u2h(a.z), u2h(o.z)));
+        a.w = h2u(__hadd2(u2h(a.w), u2h(o.w)));
+      }
+      a.x = h2u(__hmin2(__hmax2(u2h(a.x), lo), hi));
+      a.y = h2u(__hmin2(__hmax2(u2h(a.y), lo), hi));
+      a.z = h2u(__hmin2(__hmax2(u2h(a.z), lo), hi));
+      a.w = h2u(__hmin2(__hmax2(u2h(a.w), lo), hi));
+      t4[v] = a;
+    }
+  } else {
+    for (int v = t; v < S::NV; v += S::NT) {
+      __half2 acc = u2h(tot[v]);
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * S::NV + v]));
+      tot[v] = h2u(__hmin2(__hmax2(acc, lo), hi));
+    }
+  }
+  __syncthreads();
 }
 
 template <class G, int Z, int R, int SPLIT>
@@ -121,206 +301,171 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
   const float *rowB = hasB ? rowA + P.n : rowA;
   const __half2 al2 = __float2half2_rn(alpha);
   const bool scaled = alpha != 1.0f;
+  auto chan_word = [&](int v) {
+    return h2u(__floats2half2_rn(chan_value(P, rowA, v), hasB ? chan_value(P, rowB, v) : 40.0f));
+  };
 
   for (int v = t; v < S::NV; v += S::NT) {
-    const float a = chan_value(P, rowA, v);
-    const float bb = hasB ? chan_value(P, rowB, v) : 40.0f;
-    const uint32_t w = h2u(__floats2half2_rn(a, bb));
+    const uint32_t w = chan_word(v);
     if constexpr (S::CHN_SMEM) chn[v] = w;
     tot[v] = w;
   }
-  uint32_t M1[S::NR], M2[S::NR], IX[S::NR], SG[S::NR], SG2[S::NR];
+  H2State<S::NR> st;
 #pragma unroll
-  for (int j = 0; j < S::NR; ++j) {
-    M1[j] = 0u;
-    M2[j] = 0u;
-    IX[j] = 0u;
-    SG[j] = 0u;
-    SG2[j] = 0u;
-  }
+  for (int j = 0; j < S::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
   __syncthreads();
 
   int doneA = 0, doneB = hasB ? 0 : 1;
   for (int it = 0; it < num_iter; ++it) {
-    // ------------------------------------------------ check-node phase
-    uint32_t synx = 0;
-    if (lane) {
-      sfor<0, SPLIT>([&](auto hc) {
-        constexpr int H = decltype(hc)::value;
-        if (h != H) return;
-        const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
-        sfor<0, S::NR>([&](auto jc) {
-          constexpr int j = decltype(jc)::value;
-          constexpr int r = j * SPLIT + H;
-          if constexpr (r < R) {
-            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            constexpr bool packed = d <= 16;
-            // ALU-pipe relief: the min1/min2 select and the argmin update
-            // are fp16 FMAs on 1.0/0.0 compare results (FMA pipe), and the
-            // sign-bit shift is an IMAD.HI
-            const __half2 o1 = u2h(M1[j]), od = u2h(M2[j]), oix = u2h(IX[j]);
-            const uint32_t osg = SG[j], osg2 = SG2[j];
-            uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u;
-            __half2 nix = u2h(0u);
-            sfor<e0, e1>([&](auto ec) {
-              constexpr int e = decltype(ec)::value;
-              constexpr int p = e - e0;
-              const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + vn_off<G, Z, e>(i4));
-              hs ^= tw;
-              const __half2 pp = u2h(h2_int<p>());
-              const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
-              uint32_t sgn;
-              if constexpr (packed) {
-                sgn = (osg << (15 - p)) & 0x80008000u;
-              } else {
-                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
-              }
-              const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
-              const uint32_t xw = h2u(x);
-              const __half2 a = __habs2(x);
-              nix = __hfma2(__hlt2(a, u2h(n1)), __hsub2(pp, nix), nix);
-              n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
-              n1 = h2u(__hmin2(u2h(n1), a));
-              if constexpr (packed) {
-                if constexpr (p == 15)
-                  sg |= xw & 0x80008000u;
-                else
-                  sg |= __umulhi(xw, 1u << (17 + p)) & (0x10001u << p);  // xw >> (15 - p)
-              } else {
-                sg |= ((xw >> 15) & 1u) << p;
-                sg2 |= (xw >> 31) << p;
-              }
-            });
-            constexpr uint32_t dm = (1u << d) - 1u;
-            uint32_t flip;
-            if constexpr (packed) {
-              const uint32_t pa = __popc(sg & 0xFFFFu) & 1u, pb = __popc(sg >> 16) & 1u;
-              flip = ((0u - pa) & dm) | ((0u - pb) & (dm << 16));
-              SG[j] = sg ^ flip;
-            } else {
-              const uint32_t pa = __popc(sg) & 1u, pb = __popc(sg2) & 1u;
-              SG[j] = sg ^ ((0u - pa) & dm);
-              SG2[j] = sg2 ^ ((0u - pb) & dm);
-            }
-            if (scaled) {
-              n1 = h2u(__hmul2(u2h(n1), al2));
-              n2 = h2u(__hmul2(u2h(n2), al2));
-            }
-            // state keeps min1 and the fp16 difference min2 - min1; the
-            // argmin edge is reconstructed as min1 + diff (within 1 ulp of min2)
-            M1[j] = n1;
-            M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
-            IX[j] = h2u(nix);
-            synx |= hs;
-          }
-        });
-      });
-    }
+    const uint32_t synx = h2_cn<G, Z, R, SPLIT>(st, base, h, lane, al2, scaled);
     if (early_stop && it > 0) {
       // per-codeword syndrome of the posterior left by iteration `it`
       const int badA = __syncthreads_or(lane && ((synx >> 15) & 1u));
       const int badB = __syncthreads_or(lane && (synx >> 31));
       if (!doneA && !badA) {
-        h2_emit<S::NT, 0>(P, tot, S::NV, cwA, rowA, it, hard_k, llr_out, iters_used, ref, counts, red);
+        h2_emit<S::NT>(P, tot, S::NV, cwA, rowA, 0, it, hard_k, llr_out, iters_used, ref, counts, red);
         doneA = 1;
       }
       if (!doneB && !badB) {
-        h2_emit<S::NT, 1>(P, tot, S::NV, cwB, rowB, it, hard_k, llr_out, iters_used, ref, counts, red);
+        h2_emit<S::NT>(P, tot, S::NV, cwB, rowB, 1, it, hard_k, llr_out, iters_used, ref, counts, red);
         doneB = 1;
       }
       if (doneA && doneB) return;
     } else {
       __syncthreads();
     }
-    // ------------------------------------------------ variable-node phase
-    if constexpr (S::CHN_SMEM && S::NV % 4 == 0) {
-      // 128-bit shared accesses: 4 posteriors (8 messages) per instruction
-      uint4 *t4 = reinterpret_cast<uint4 *>(tot);
-      const uint4 *c4 = reinterpret_cast<const uint4 *>(chn);
-      for (int v = t; v < S::NV / 4; v += S::NT) {
-        t4[v] = c4[v];
-#pragma unroll
-        for (int q = 1; q < SPLIT; ++q) t4[q * (S::NV / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
-      }
-    } else {
-      for (int v = t; v < S::NV; v += S::NT) {
-        uint32_t ch;
-        if constexpr (S::CHN_SMEM) {
-          ch = chn[v];
-        } else {
-          ch = h2u(__floats2half2_rn(chan_value(P, rowA, v), hasB ? chan_value(P, rowB, v) : 40.0f));
-        }
-        tot[v] = ch;
-#pragma unroll
-        for (int q = 1; q < SPLIT; ++q) tot[q * S::NV + v] = 0u;
-      }
-    }
-    __syncthreads();
-    sfor<0, S::NR>([&](auto jc) {
-      constexpr int j = decltype(jc)::value;
-      if (lane) {
-        sfor<0, SPLIT>([&](auto hc) {
-          constexpr int H = decltype(hc)::value;
-          constexpr int r = j * SPLIT + H;
-          if constexpr (r < R) {
-            if (h != H) return;
-            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            constexpr bool packed = d <= 16;
-            const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
-            char *const arr = base + 4u * H * S::NV;
-            const __half2 o1 = u2h(M1[j]), od = u2h(M2[j]), oix = u2h(IX[j]);
-            const uint32_t osg = SG[j], osg2 = SG2[j];
-            sfor<e0, e1>([&](auto ec) {
-              constexpr int e = decltype(ec)::value;
-              constexpr int p = e - e0;
-              uint32_t *tp = reinterpret_cast<uint32_t *>(arr + vn_off<G, Z, e>(i4));
-              const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-              uint32_t sgn;
-              if constexpr (packed) {
-                sgn = (osg << (15 - p)) & 0x80008000u;
-              } else {
-                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
-              }
-              *tp = h2u(__hadd2(u2h(*tp), u2h(mag | sgn)));
-            });
-          }
-        });
-      }
-      __syncthreads();
-    });
-    const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
-    if constexpr (S::NV % 4 == 0) {
-      uint4 *t4 = reinterpret_cast<uint4 *>(tot);
-      for (int v = t; v < S::NV / 4; v += S::NT) {
-        uint4 a = t4[v];
-#pragma unroll
-        for (int q = 1; q < SPLIT; ++q) {
-          const uint4 o = t4[q * (S::NV / 4) + v];
-          a.x = h2u(__hadd2(u2h(a.x), u2h(o.x)));
-          a.y = h2u(__hadd2(u2h(a.y), u2h(o.y)));
-          a.z = h2u(__hadd2(u2h(a.z), u2h(o.z)));
-          a.w = h2u(__hadd2(u2h(a.w), u2h(o.w)));
-        }
-        a.x = h2u(__hmin2(__hmax2(u2h(a.x), lo), hi));
-        a.y = h2u(__hmin2(__hmax2(u2h(a.y), lo), hi));
-        a.z = h2u(__hmin2(__hmax2(u2h(a.z), lo), hi));
-        a.w = h2u(__hmin2(__hmax2(u2h(a.w), lo), hi));
-        t4[v] = a;
-      }
-    } else {
-      for (int v = t; v < S::NV; v += S::NT) {
-        __half2 acc = u2h(tot[v]);
-#pragma unroll
-        for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * S::NV + v]));
-        tot[v] = h2u(__hmin2(__hmax2(acc, lo), hi));
-      }
-    }
-    __syncthreads();
+    h2_vn<G, Z, R, SPLIT>(st, tot, chn, base, h, lane, t, chan_word);
   }
-  if (!doneA) h2_emit<S::NT, 0>(P, tot, S::NV, cwA, rowA, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
-  if (!doneB) h2_emit<S::NT, 1>(P, tot, S::NV, cwB, rowB, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+  if (!doneA) h2_emit<S::NT>(P, tot, S::NV, cwA, rowA, 0, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+  if (!doneB) h2_emit<S::NT>(P, tot, S::NV, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+}
+
+// zero the check state of the refilled half(s): packed rows keep A in the low
+// and B in the high halves of every word; unpacked rows keep B's signs in SG2
+template <class G, int Z, int R, int SPLIT, int NR>
+__device__ __forceinline__ void h2_reset_half(H2State<NR> &st, int h, int new0, int new1) {
+  const uint32_t keep = (new0 ? 0xFFFF0000u : 0xFFFFFFFFu) & (new1 ? 0x0000FFFFu : 0xFFFFFFFFu);
+  sfor<0, SPLIT>([&](auto hc) {
+    constexpr int H = decltype(hc)::value;
+    if (h != H) return;
+    sfor<0, NR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      constexpr int r = j * SPLIT + H;
+      if constexpr (r < R) {
+        constexpr int d = G::row_start[r + 1] - G::row_start[r];
+        st.M1[j] &= keep;
+        st.M2[j] &= keep;
+        st.IX[j] &= keep;
+        if constexpr (d <= 16) {
+          st.SG[j] &= keep;
+        } else {
+          if (new0) st.SG[j] = 0u;
+          if (new1) st.SG2[j] = 0u;
+        }
+      }
+    });
+  });
+}
+
+// Persistent early-stop variant: one CTA per SM keeps two codeword slots (the
+// low / high fp16 halves) busy.  When a slot's codeword converges (or reaches
+// num_iter) its outputs are written and the slot is refilled with the next
+// codeword from a global counter, so a converged codeword no longer idles
+// while its partner keeps iterating.  Same per-codeword arithmetic and
+// iteration semantics as k_qc_fast_h2 (the halves never interact).
+template <class G, int Z, int R, int SPLIT>
+__global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
+    k_qc_fast_h2p(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
+                  uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
+                  const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts,
+                  unsigned long long *__restrict__ next) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  static_assert(S::CHN_SMEM, "the persistent decoder refills the cached channel LLRs per slot");
+  extern __shared__ uint32_t smw[];
+  uint32_t *tot = smw;
+  uint32_t *chn = smw + SPLIT * S::NV;
+  __shared__ unsigned red[S::NT / 32];
+  __shared__ long long slot_cw[2];
+  __shared__ int slot_it[2], slot_new[2];
+  const int t = threadIdx.x;
+  const int h = t / S::NT1;
+  const int i = t - h * S::NT1;
+  const bool lane = i < Z;
+  char *const base = reinterpret_cast<char *>(smw);
+  const __half2 al2 = __float2half2_rn(alpha);
+  const bool scaled = alpha != 1.0f;
+  H2State<S::NR> st;
+#pragma unroll
+  for (int j = 0; j < S::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+  if (t == 0) {
+    slot_cw[0] = slot_cw[1] = -1;
+    slot_it[0] = slot_it[1] = 0;
+  }
+  __syncthreads();
+  auto chan_word = [&](int v) { return chn[v]; };  // unused: CHN_SMEM
+  for (;;) {
+    // ---- refill empty slots
+    if (t == 0) {
+      for (int q = 0; q < 2; ++q) {
+        slot_new[q] = 0;
+        if (slot_cw[q] < 0) {
+          const unsigned long long c = atomicAdd(next, 1ULL);
+          if ((long long)c < batch) {
+            slot_cw[q] = (long long)c;
+            slot_it[q] = 0;
+            slot_new[q] = 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const long long cw0 = slot_cw[0], cw1 = slot_cw[1];
+    if (cw0 < 0 && cw1 < 0) return;
+    const int new0 = slot_new[0], new1 = slot_new[1];
+    if (new0 | new1) {
+      unsigned short *c16 = reinterpret_cast<unsigned short *>(chn);
+      unsigned short *t16 = reinterpret_cast<unsigned short *>(tot);
+      for (int q = 0; q < 2; ++q) {
+        if (!(q ? new1 : new0)) continue;
+        const float *row = llr + (q ? cw1 : cw0) * (int64_t)P.n;
+        for (int v = t; v < S::NV; v += S::NT) {
+          const unsigned short hv = __half_as_ushort(__float2half_rn(chan_value(P, row, v)));
+          c16[2 * v + q] = hv;
+          t16[2 * v + q] = hv;
+        }
+      }
+      // fresh check state for the refilled half (the other half continues)
+      h2_reset_half<G, Z, R, SPLIT>(st, h, new0, new1);
+      __syncthreads();
+    }
+    // ---- one iteration for both slots
+    const uint32_t synx = h2_cn<G, Z, R, SPLIT>(st, base, h, lane, al2, scaled);
+    const int bad0 = __syncthreads_or(lane && ((synx >> 15) & 1u));
+    const int bad1 = __syncthreads_or(lane && (synx >> 31));
+    bool freed = false;
+    for (int q = 0; q < 2; ++q) {
+      const long long cw = q ? cw1 : cw0;
+      if (cw < 0) continue;
+      const int itq = slot_it[q];
+      const bool conv = itq > 0 && !(q ? bad1 : bad0);
+      if (conv || itq == num_iter) {
+        h2_emit<S::NT>(P, tot, S::NV, cw, llr + cw * (int64_t)P.n, q, itq, hard_k, llr_out, iters_used, ref,
+                       counts, red);
+        __syncthreads();
+        if (t == 0) slot_cw[q] = -1;
+        freed = true;
+      }
+    }
+    if (freed) {
+      __syncthreads();
+      if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
+    }
+    h2_vn<G, Z, R, SPLIT>(st, tot, chn, base, h, lane, t, chan_word);
+    if (t == 0) {
+      slot_it[0] += 1;
+      slot_it[1] += 1;
+    }
+  }
 }
 
 template <class G, int Z, int R, int SPLIT>
@@ -328,8 +473,30 @@ int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int nu
                       uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
                       unsigned long long *counts, cudaStream_t s) {
   using S = QcShapeH2<G, Z, R, SPLIT>;
+  cudaError_t e;
+  if constexpr (S::CHN_SMEM) {
+    if (early_stop && B >= 4) {  // persistent slot-refilling decoder
+      auto kp = k_qc_fast_h2p<G, Z, R, SPLIT>;
+      e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, S::NT, S::SMEM);
+      const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
+      unsigned long long *next = nullptr;
+      e = cudaMallocAsync((void **)&next, sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(counter)");
+      cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+      kp<<<(unsigned)grid, S::NT, S::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, llr_out, iters_used, ref, counts,
+                                                next);
+      e = cudaGetLastError();
+      cudaFreeAsync(next, s);
+      return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+    }
+  }
   auto kern = k_qc_fast_h2<G, Z, R, SPLIT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   const int64_t chunk = 2LL * 0x3fffffff;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {

@@ -331,6 +331,30 @@ def test_fast_sum_product_decoder(k, n, m, ebno, es):
         assert (it == 20).all()
 
 
+def test_fast_decoders_agree_on_a_large_batch():
+    """fp32, fp16x2 (pair and persistent slot-refilling kernels) on 1184
+    config-2 codewords at 6 dB: every variant decodes the same blocks."""
+    cfg = lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": 8448, "n": 16896},
+                                  "modulation": {"kind": "qam", "bits_per_symbol": 4},
+                                  "sweep": {"ebno_db": [6.0], "batch_size": 1184}})
+    pipe = lb.Pipeline(cfg)
+    payload, llr = pipe._llr(6.0, 1184, lb.RngStream(1, 2))
+    bad = {}
+    for prec in ("fp32", "fp16x2"):
+        for es in (False, True):
+            r = lb.qc_decode(llr, pipe.ldpc, 20, "min-sum", early_stop=es, ref_bits=payload, precision=prec,
+                             want_iters=True)
+            bad[(prec, es)] = (r["hard"] != payload).any(dim=1).cpu().numpy()
+            it = r["iters"].cpu().numpy()
+            assert (it >= 1).all() and (it <= 20).all()
+            if es:
+                assert it.mean() < 12
+    ref = bad[("fp32", False)]
+    assert ref.sum() <= 12
+    for key, b in bad.items():
+        assert (b != ref).sum() <= 4, key
+
+
 def test_fast_decoder_noiseless_round_trip_and_early_stop():
     for k, n in [(500, 1000), (100, 300), (8448, 16896), (4096, 12288), (256, 1536)]:
         code = lb.LdpcCode5G(k, n)
