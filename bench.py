@@ -316,7 +316,8 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s",
             "mean_iterations": mean_it, "ms_per_step": ms / steps,
             "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
-            "note": "fp16x2 kernel pairs two codewords per CTA: a pair runs until both converge"}
+            "note": "persistent fp16x2 kernel: each SM keeps two codeword slots busy and refills a slot "
+                    "as soon as its codeword's syndrome is satisfied"}
 
 
 def _wall_max(dist, secs):

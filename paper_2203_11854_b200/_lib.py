@@ -130,24 +130,26 @@ def is_tensor(x) -> bool:
 
 
 def to_device(x, dtype=None):
-    """numpy/array-like -> contiguous CUDA tensor (H2D via pinned staging)."""
+    """numpy/array-like or tensor -> contiguous CUDA tensor of `dtype`.
+
+    Host tensors are copied as they are (asynchronously when pinned) and
+    converted on the device; numpy arrays are converted on the host (never
+    widening the transfer) and copied from pageable memory -- pinning a fresh
+    staging buffer per call costs more than it saves.
+    """
     t = torch()
     dev = device()
     if is_tensor(x):
         y = x
-        if dtype is not None and y.dtype != getattr(t, dtype):
-            y = y.to(getattr(t, dtype))
         if y.device != dev:
             y = y.to(dev, non_blocking=True)
+        if dtype is not None and y.dtype != getattr(t, dtype):
+            y = y.to(getattr(t, dtype))
         return y.contiguous()
     a = np.asarray(x)
     if dtype is not None:
         a = a.astype(dtype, copy=False)
-    a = np.ascontiguousarray(a)
-    host = t.from_numpy(a)
-    if a.nbytes >= (1 << 20):
-        host = host.pin_memory()
-    return host.to(dev, non_blocking=True)
+    return t.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
 def to_host(t):

@@ -18,11 +18,9 @@ import io
 import time
 from dataclasses import dataclass, field
 
-import numpy as np
-
 from . import _lib as L
 from .channel import awgn
-from .core import RngStream, binary_source, count_errors, ebnodb2no
+from .core import RngStream, binary_source, ebnodb2no
 from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode, qc_has_kernel
 from .mapping import Constellation, demap_app, demap_maxlog, map_bits, modem_qam
 
