@@ -24,6 +24,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
 
 
 GEN = os.path.join(ROOT, "build", "gen")
+# per-source extra flags: the numpy-replica RNG must round every operation
+# separately, as the host libm/numpy code it mirrors does
+EXTRA = {"rng_normal.cu": ["-fmad=false"]}
 
 
 def _instance_sources():
@@ -58,7 +61,7 @@ def _compile(src: str, verbose: bool, newest_hdr: float, force: bool) -> str:
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_hdr)):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
