@@ -288,10 +288,16 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
     counts = L.zeros((2,), "int64")
     iters = []
 
+    dec = []
+
     def one(i):
         payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (900 + i)))
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        dec.append((d0, d1))
         r = lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=True, ref_bits=payload,
                          want_hard=False, want_iters=True, counts=counts, precision=pipe.precision)
+        d1.record()
         iters.append(r["iters"])
 
     one(-1)
@@ -300,12 +306,14 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters.clear()
+    dec.clear()
     counts.zero_()
-    e0.record()
-    for i in range(steps):
-        one(i)
-    e1.record()
-    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        e0.record()
+        for i in range(steps):
+            one(i)
+        e1.record()
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
@@ -314,7 +322,8 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
     mean_it = float(torch.cat(iters).float().mean())
     c = counts.cpu().tolist()
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s",
-            "mean_iterations": mean_it, "ms_per_step": ms / steps,
+            "mean_iterations": mean_it, "ms_per_step": ms / steps, "clocks": clk.summary(),
+            "decoder_ms_per_launch": sum(d0.elapsed_time(d1) for d0, d1 in dec) / steps,
             "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
             "note": "persistent fp16x2 kernel: each SM keeps two codeword slots busy and refills a slot "
                     "as soon as its codeword's syndrome is satisfied"}
