@@ -164,7 +164,10 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
  * counts[2] += (bit errors, block errors) against ref_bits [B,k].
  * flags: LS_QC_PRUNE skips the dead extension rows whose parity bit is never
  * transmitted (their llr_out entries are then the channel values);
- * LS_QC_GENERIC forces the runtime-Z kernel instead of a specialised one. */
+ * LS_QC_GENERIC forces a runtime-geometry kernel instead of a specialised
+ * one (fp32: the runtime-Z kernel; with LS_QC_FP16: the runtime-geometry
+ * fp16x2 kernel, which is also what LS_QC_FP16 uses when no specialised
+ * instance exists). */
 #define LS_QC_PRUNE 1
 #define LS_QC_GENERIC 2
 #define LS_QC_FP16 4 /* packed fp16x2 kernel: two codewords per 32-bit lane */

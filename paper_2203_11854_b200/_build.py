@@ -46,12 +46,25 @@ def _instance_sources():
                 "    uint8_t *h, float *lo, int32_t *iu, const uint8_t *ref, unsigned long long *cnt, cudaStream_t s) {\n"
                 f"  return {launcher}<BG{bg}Tables, {z}, {r}, {sp}>(P, l, B, it, a, es, h, lo, iu, ref, cnt, s);\n"
                 "}\n}  // namespace lsb\n")
-        path = os.path.join(GEN, name)
-        if not os.path.exists(path) or open(path).read() != body:
-            with open(path, "w") as f:
-                f.write(body)
-        out.append(path)
+        out.append(_write(name, body))
+    for bg, rb, sp in re.findall(r"Y\((\d+),\s*(\d+),\s*(\d+)\)", text):
+        body = (f'#include "{CSRC}/bp_fast_h2.cuh"\n'
+                "namespace lsb {\n"
+                f"int qcrt_{bg}_{rb}_{sp}(const QcChanParams &P, int R, const uint16_t *s, const int32_t *col,\n"
+                "    const float *l, int64_t B, int it, float a, int es, uint8_t *h, float *lo, int32_t *iu,\n"
+                "    const uint8_t *ref, unsigned long long *cnt, cudaStream_t st) {\n"
+                f"  return launch_qc_h2rt<BG{bg}Tables, {rb}, {sp}>(P, R, s, col, l, B, it, a, es, h, lo, iu, ref, cnt, st);\n"
+                "}\n}  // namespace lsb\n")
+        out.append(_write(f"qcrt_{bg}_{rb}_{sp}.cu", body))
     return out
+
+
+def _write(name: str, body: str) -> str:
+    path = os.path.join(GEN, name)
+    if not os.path.exists(path) or open(path).read() != body:
+        with open(path, "w") as f:
+            f.write(body)
+    return path
 
 
 

@@ -223,6 +223,33 @@ LSB_QC_INSTANCES(LSB_QC_DECL)
 #define LSB_QC_ENTRY(bg, z, r, sp, pr) {bg, z, r, LSB_QC_PREC_##pr, &qc2_##pr##_##bg##_##z##_##r},
 static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
 
+typedef int (*QcRtFn)(const QcChanParams &, int, const uint16_t *, const int32_t *, const float *, int64_t, int,
+                      float, int, uint8_t *, float *, int32_t *, const uint8_t *, unsigned long long *,
+                      cudaStream_t);
+#define LSB_QC_RT_DECL(bg, rb, sp)                                                                           \
+  int qcrt_##bg##_##rb##_##sp(const QcChanParams &, int, const uint16_t *, const int32_t *, const float *, \
+                              int64_t, int, float, int, uint8_t *, float *, int32_t *, const uint8_t *,    \
+                              unsigned long long *, cudaStream_t);
+LSB_QC_RT_INSTANCES(LSB_QC_RT_DECL)
+struct QcRtEntry {
+  int bg, rb, split;
+  QcRtFn fn;
+};
+#define LSB_QC_RT_ENTRY(bg, rb, sp) {bg, rb, sp, &qcrt_##bg##_##rb##_##sp},
+static const QcRtEntry kQcRtKernels[] = {LSB_QC_RT_INSTANCES(LSB_QC_RT_ENTRY)};
+
+// runtime-geometry fp16x2 instance for (BG, Z, R): smallest row bound >= R,
+// then the most threads per lane that fit 768 threads
+static const QcRtEntry *pick_rt(int bg, int z, int R) {
+  const QcRtEntry *best = nullptr;
+  const int nt1 = ((z + 31) / 32) * 32;
+  for (const QcRtEntry &k : kQcRtKernels) {
+    if (k.bg != bg || k.rb < R || nt1 * k.split > 768) continue;
+    if (!best || k.rb < best->rb || (k.rb == best->rb && k.split > best->split)) best = &k;
+  }
+  return best;
+}
+
 // rows whose degree-1 extension column holds at least one transmitted bit:
 // the transmitted mother positions are a prefix of the circular buffer
 // (ldpc.py:252-256), so the live rows are a prefix 0..R-1
@@ -245,6 +272,7 @@ extern "C" int ls_qc_has_kernel(const ls_code *code, int flags) {
   if (!code) return 0;
   const int R = (flags & LS_QC_PRUNE) ? live_rows(code->p) : code->p.mb;
   const int prec = (flags & LS_QC_SP) ? 2 : qc_kind(LS_MIN_SUM, flags);
+  if (!code->std_shifts) return 0;
   for (const QcKernelEntry &k : kQcKernels)
     if (k.bg == code->p.bg && k.z == code->p.z && k.r == R && k.prec == prec) return 1;
   return 0;
@@ -262,20 +290,26 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
   const int prec = qc_kind(variant, flags);
-  if (prec && (flags & LS_QC_GENERIC))
-    return fail(LS_EINVAL, "ls_qc_decode: the fp16x2 and sum-product decoders have no runtime-Z kernel");
-  if (!(flags & LS_QC_GENERIC)) {
-    const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
+  if (prec == 2 && (flags & LS_QC_GENERIC))
+    return fail(LS_EINVAL, "ls_qc_decode: the sum-product fast decoder has no runtime-Z kernel");
+  const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
+  const QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
+  if (!(flags & LS_QC_GENERIC) && code->std_shifts) {
     for (const QcKernelEntry &k : kQcKernels) {
-      if (k.bg == P.bg && k.z == P.z && k.r == R && k.prec == prec) {
-        QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
+      if (k.bg == P.bg && k.z == P.z && k.r == R && k.prec == prec)
         return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
-      }
     }
-    if (prec == 1) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
-    if (prec == 2)
-      return fail(LS_EINVAL, "ls_qc_decode: no sum-product fast decoder instance for this (BG, Z, rows); "
-                             "use the exact decoder");
+  }
+  if (prec == 2)
+    return fail(LS_EINVAL, "ls_qc_decode: no sum-product fast decoder instance for this (BG, Z, rows); "
+                           "use the exact decoder");
+  if (prec == 1) {  // fp16x2 at any (Z, R): runtime-geometry instance
+    const QcRtEntry *k = pick_rt(P.bg, P.z, R);
+    if (!k) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
+    int32_t col[kMaxNnz];
+    for (int e = 0; e < P.nnz; ++e) col[e] = code->entries[3 * e + 1];
+    return k->fn(CP, R, P.s, col, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits,
+                 counts, s);
   }
   QcFastParams FP;
   FP.z = P.z; FP.k = P.k; FP.n = P.n; FP.k_full = P.k_full; FP.n_full = P.n_full; FP.l1 = P.l1;

@@ -55,9 +55,60 @@ struct QcShapeH2 {
   static constexpr int MINB = NT >= 384 ? 1 : (384 / NT);
 };
 
+// Geometry policies.  The phase functions and kernels below are written once
+// against a policy `Geo`:
+//   H2GeoCT<G, Z, R, SPLIT>  everything compile-time (the specialised
+//                            instances of qc_instances.h): shifts, column
+//                            bases and loop bounds are immediates;
+//   H2GeoRT<G, RB, SPLIT>    base-graph structure and a row bound RB
+//                            compile-time; Z, the processed rows R <= RB and
+//                            the per-edge shift / column offsets are runtime
+//                            values held in the kernel's parameter space, so
+//                            they are constant-bank operands (one extra IADD
+//                            per edge visit against the immediate form).
+template <class G_, int Z, int R, int SPLIT_>
+struct H2GeoCT {
+  using G = G_;
+  using S = QcShapeH2<G_, Z, R, SPLIT_>;
+  static constexpr int SPLIT = SPLIT_, RB = R, NR = S::NR, NT_MAX = S::NT, MINB = S::MINB;
+  __device__ __forceinline__ static constexpr int nt1() { return S::NT1; }
+  __device__ __forceinline__ static constexpr int nt() { return S::NT; }
+  __device__ __forceinline__ static constexpr int nv() { return S::NV; }
+  __device__ __forceinline__ static constexpr bool chn_smem() { return S::CHN_SMEM; }
+  __device__ __forceinline__ static constexpr int z() { return Z; }
+  template <int r>
+  __device__ __forceinline__ static constexpr bool live() { return true; }
+  template <int e>
+  __device__ __forceinline__ static unsigned off(unsigned i4) { return vn_off<G_, Z, e>(i4); }
+};
+
+template <class G_, int RB_, int SPLIT_>
+struct H2GeoRT {
+  using G = G_;
+  static constexpr int SPLIT = SPLIT_, RB = RB_, NR = (RB_ + SPLIT_ - 1) / SPLIT_;
+  static constexpr int NE = G_::row_start[RB_];  // edges of rows < RB
+  static constexpr int NT_MAX = 768, MINB = 1;   // Z <= 384 / SPLIT * 2 (launcher checks)
+  int Z, NT1, NT, NV, R, CHN;
+  unsigned Z4;
+  uint32_t s4[NE];  // 4 * (shift mod Z)
+  uint32_t cb[NE];  // 4 * Z * column
+  __device__ __forceinline__ int nt1() const { return NT1; }
+  __device__ __forceinline__ int nt() const { return NT; }
+  __device__ __forceinline__ int nv() const { return NV; }
+  __device__ __forceinline__ bool chn_smem() const { return CHN != 0; }
+  __device__ __forceinline__ int z() const { return Z; }
+  template <int r>
+  __device__ __forceinline__ bool live() const { return r < R; }
+  template <int e>
+  __device__ __forceinline__ unsigned off(unsigned i4) const {
+    const unsigned u = i4 + s4[e];
+    return cb[e] + min(u, u - Z4);
+  }
+};
+
 // per-codeword outputs of half `hb` (0 = A, 1 = B) from the current posteriors
-template <int NT>
-__device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *tot, int nv, int64_t cw,
+template <int NT_MAX>
+__device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *tot, int nv, int NT, int64_t cw,
                                         const float *row, int hb, int used, uint8_t *hard_k, float *llr_out,
                                         int32_t *iters_used, const uint8_t *ref, unsigned long long *counts,
                                         unsigned *red) {
@@ -91,7 +142,7 @@ __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *t
     __syncthreads();
     if (t == 0) {
       unsigned long long tt = 0;
-      for (int w = 0; w < NT / 32; ++w) tt += red[w];
+      for (int w = 0; w < (NT + 31) / 32; ++w) tt += red[w];
       if (tt) {
         atomicAdd(&counts[0], tt);
         atomicAdd(&counts[1], 1ULL);
@@ -110,20 +161,22 @@ struct H2State {
 
 // Check-node phase of one iteration for the calling thread's rows; returns
 // the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B).
-template <class G, int Z, int R, int SPLIT, int NR>
-__device__ __forceinline__ uint32_t h2_cn(H2State<NR> &st, const char *base, int h, bool lane, __half2 al2,
-                                         bool scaled) {
-  using S = QcShapeH2<G, Z, R, SPLIT>;
+template <class Geo>
+__device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base, int h, bool lane, __half2 al2,
+                                         bool scaled, const Geo &geo) {
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
   uint32_t synx = 0;
   if (!lane) return 0;
   sfor<0, SPLIT>([&](auto hc) {
     constexpr int H = decltype(hc)::value;
     if (h != H) return;
-    const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
+    const unsigned i4 = 4u * tid_volatile() - 4u * H * geo.nt1();
     sfor<0, NR>([&](auto jc) {
       constexpr int j = decltype(jc)::value;
       constexpr int r = j * SPLIT + H;
-      if constexpr (r < R) {
+      if constexpr (r < Geo::RB) {
+        if (!geo.template live<r>()) return;
         constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
         constexpr bool packed = d <= 16;
         // ALU-pipe relief: the min1/min2 select and the argmin update are
@@ -135,7 +188,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<NR> &st, const char *base, int
         sfor<e0, e1>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int p = e - e0;
-          const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + vn_off<G, Z, e>(i4));
+          const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
           hs ^= tw;
           const __half2 pp = u2h(h2_int<p>());
           const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
@@ -189,30 +242,26 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<NR> &st, const char *base, int
 
 // Variable-node phase: posteriors = clip(chan + sum of the new messages).
 // `chan_word(v)` supplies the channel half2 of VN v when it is not cached.
-template <class G, int Z, int R, int SPLIT, int NR, class ChanFn>
-__device__ __forceinline__ void h2_vn(const H2State<NR> &st, uint32_t *tot, const uint32_t *chn, char *base, int h,
-                                      bool lane, int t, ChanFn chan_word) {
-  using S = QcShapeH2<G, Z, R, SPLIT>;
-  if constexpr (S::CHN_SMEM && S::NV % 4 == 0) {
+template <class Geo, class ChanFn>
+__device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot, const uint32_t *chn, char *base,
+                                      int h, bool lane, int t, ChanFn chan_word, const Geo &geo) {
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
+  const int NV = geo.nv(), NT = geo.nt();
+  if (geo.chn_smem() && NV % 4 == 0) {
     // 128-bit shared accesses: 4 posteriors (8 messages) per instruction
     uint4 *t4 = reinterpret_cast<uint4 *>(tot);
     const uint4 *c4 = reinterpret_cast<const uint4 *>(chn);
-    for (int v = t; v < S::NV / 4; v += S::NT) {
+    for (int v = t; v < NV / 4; v += NT) {
       t4[v] = c4[v];
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) t4[q * (S::NV / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
+      for (int q = 1; q < SPLIT; ++q) t4[q * (NV / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
     }
   } else {
-    for (int v = t; v < S::NV; v += S::NT) {
-      uint32_t ch;
-      if constexpr (S::CHN_SMEM) {
-        ch = chn[v];
-      } else {
-        ch = chan_word(v);
-      }
-      tot[v] = ch;
+    for (int v = t; v < NV; v += NT) {
+      tot[v] = geo.chn_smem() ? chn[v] : chan_word(v);
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) tot[q * S::NV + v] = 0u;
+      for (int q = 1; q < SPLIT; ++q) tot[q * NV + v] = 0u;
     }
   }
   __syncthreads();
@@ -222,18 +271,18 @@ __device__ __forceinline__ void h2_vn(const H2State<NR> &st, uint32_t *tot, cons
       sfor<0, SPLIT>([&](auto hc) {
         constexpr int H = decltype(hc)::value;
         constexpr int r = j * SPLIT + H;
-        if constexpr (r < R) {
-          if (h != H) return;
+        if constexpr (r < Geo::RB) {
+          if (h != H || !geo.template live<r>()) return;
           constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
           constexpr bool packed = d <= 16;
-          const unsigned i4 = 4u * tid_volatile() - 4u * H * S::NT1;
-          char *const arr = base + 4u * H * S::NV;
+          const unsigned i4 = 4u * tid_volatile() - 4u * H * geo.nt1();
+          char *const arr = base + 4u * H * NV;
           const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
           const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
           sfor<e0, e1>([&](auto ec) {
             constexpr int e = decltype(ec)::value;
             constexpr int p = e - e0;
-            uint32_t *tp = reinterpret_cast<uint32_t *>(arr + vn_off<G, Z, e>(i4));
+            uint32_t *tp = reinterpret_cast<uint32_t *>(arr + geo.template off<e>(i4));
             const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
             uint32_t sgn;
             if constexpr (packed) {
@@ -250,13 +299,13 @@ __device__ __forceinline__ void h2_vn(const H2State<NR> &st, uint32_t *tot, cons
     __syncthreads();
   });
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
-  if constexpr (S::NV % 4 == 0) {
+  if (NV % 4 == 0) {
     uint4 *t4 = reinterpret_cast<uint4 *>(tot);
-    for (int v = t; v < S::NV / 4; v += S::NT) {
+    for (int v = t; v < NV / 4; v += NT) {
       uint4 a = t4[v];
 #pragma unroll
       for (int q = 1; q < SPLIT; ++q) {
-        const uint4 o = t4[q * (S::NV / 4) + v];
+        const uint4 o = t4[q * (NV / 4) + v];
         a.x = h2u(__hadd2(u2h(a.x), u2h(o.x)));
         a.y = h2u(__hadd2(u2h(a.y), u2h(o.y)));
         a.z = h2u(__hadd2(u2h(a.z), u2h(o.z)));
@@ -269,31 +318,32 @@ __device__ __forceinline__ void h2_vn(const H2State<NR> &st, uint32_t *tot, cons
       t4[v] = a;
     }
   } else {
-    for (int v = t; v < S::NV; v += S::NT) {
+    for (int v = t; v < NV; v += NT) {
       __half2 acc = u2h(tot[v]);
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * S::NV + v]));
+      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * NV + v]));
       tot[v] = h2u(__hmin2(__hmax2(acc, lo), hi));
     }
   }
   __syncthreads();
 }
 
-template <class G, int Z, int R, int SPLIT>
-__global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z, R, SPLIT>::MINB)
-    k_qc_fast_h2(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
-                 int early_stop, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
+    k_qc_fast_h2(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
+                 float alpha, int early_stop, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
                  int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
                  unsigned long long *__restrict__ counts) {
-  using S = QcShapeH2<G, Z, R, SPLIT>;
+  constexpr int SPLIT = Geo::SPLIT;
   extern __shared__ uint32_t smw[];
+  const int NV = geo.nv(), NT = geo.nt();
   uint32_t *tot = smw;
-  uint32_t *chn = smw + SPLIT * S::NV;
-  __shared__ unsigned red[S::NT / 32];
+  uint32_t *chn = smw + SPLIT * NV;
+  __shared__ unsigned red[Geo::NT_MAX / 32];
   const int t = threadIdx.x;
-  const int h = t / S::NT1;
-  const int i = t - h * S::NT1;
-  const bool lane = i < Z;
+  const int h = t / geo.nt1();
+  const int i = t - h * geo.nt1();
+  const bool lane = i < geo.z();
   char *const base = reinterpret_cast<char *>(smw);
   const int64_t cwA = 2 * (int64_t)blockIdx.x, cwB = cwA + 1;
   const bool hasB = cwB < batch;
@@ -305,45 +355,49 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, QcShapeH2<G, Z,
     return h2u(__floats2half2_rn(chan_value(P, rowA, v), hasB ? chan_value(P, rowB, v) : 40.0f));
   };
 
-  for (int v = t; v < S::NV; v += S::NT) {
+  for (int v = t; v < NV; v += NT) {
     const uint32_t w = chan_word(v);
-    if constexpr (S::CHN_SMEM) chn[v] = w;
+    if (geo.chn_smem()) chn[v] = w;
     tot[v] = w;
   }
-  H2State<S::NR> st;
+  H2State<Geo::NR> st;
 #pragma unroll
-  for (int j = 0; j < S::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+  for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
   __syncthreads();
 
   int doneA = 0, doneB = hasB ? 0 : 1;
   for (int it = 0; it < num_iter; ++it) {
-    const uint32_t synx = h2_cn<G, Z, R, SPLIT>(st, base, h, lane, al2, scaled);
+    const uint32_t synx = h2_cn(st, base, h, lane, al2, scaled, geo);
     if (early_stop && it > 0) {
       // per-codeword syndrome of the posterior left by iteration `it`
       const int badA = __syncthreads_or(lane && ((synx >> 15) & 1u));
       const int badB = __syncthreads_or(lane && (synx >> 31));
       if (!doneA && !badA) {
-        h2_emit<S::NT>(P, tot, S::NV, cwA, rowA, 0, it, hard_k, llr_out, iters_used, ref, counts, red);
+        h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwA, rowA, 0, it, hard_k, llr_out, iters_used, ref, counts, red);
         doneA = 1;
       }
       if (!doneB && !badB) {
-        h2_emit<S::NT>(P, tot, S::NV, cwB, rowB, 1, it, hard_k, llr_out, iters_used, ref, counts, red);
+        h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwB, rowB, 1, it, hard_k, llr_out, iters_used, ref, counts, red);
         doneB = 1;
       }
       if (doneA && doneB) return;
     } else {
       __syncthreads();
     }
-    h2_vn<G, Z, R, SPLIT>(st, tot, chn, base, h, lane, t, chan_word);
+    h2_vn(st, tot, chn, base, h, lane, t, chan_word, geo);
   }
-  if (!doneA) h2_emit<S::NT>(P, tot, S::NV, cwA, rowA, 0, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
-  if (!doneB) h2_emit<S::NT>(P, tot, S::NV, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+  if (!doneA)
+    h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwA, rowA, 0, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
+  if (!doneB)
+    h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
 }
 
 // zero the check state of the refilled half(s): packed rows keep A in the low
 // and B in the high halves of every word; unpacked rows keep B's signs in SG2
-template <class G, int Z, int R, int SPLIT, int NR>
-__device__ __forceinline__ void h2_reset_half(H2State<NR> &st, int h, int new0, int new1) {
+template <class Geo>
+__device__ __forceinline__ void h2_reset_half(H2State<Geo::NR> &st, int h, int new0, int new1) {
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
   const uint32_t keep = (new0 ? 0xFFFF0000u : 0xFFFFFFFFu) & (new1 ? 0x0000FFFFu : 0xFFFFFFFFu);
   sfor<0, SPLIT>([&](auto hc) {
     constexpr int H = decltype(hc)::value;
@@ -351,7 +405,7 @@ __device__ __forceinline__ void h2_reset_half(H2State<NR> &st, int h, int new0, 
     sfor<0, NR>([&](auto jc) {
       constexpr int j = decltype(jc)::value;
       constexpr int r = j * SPLIT + H;
-      if constexpr (r < R) {
+      if constexpr (r < Geo::RB) {
         constexpr int d = G::row_start[r + 1] - G::row_start[r];
         st.M1[j] &= keep;
         st.M2[j] &= keep;
@@ -372,37 +426,38 @@ __device__ __forceinline__ void h2_reset_half(H2State<NR> &st, int h, int new0, 
 // num_iter) its outputs are written and the slot is refilled with the next
 // codeword from a global counter, so a converged codeword no longer idles
 // while its partner keeps iterating.  Same per-codeword arithmetic and
-// iteration semantics as k_qc_fast_h2 (the halves never interact).
-template <class G, int Z, int R, int SPLIT>
-__global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
-    k_qc_fast_h2p(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
-                  uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
-                  const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts,
-                  unsigned long long *__restrict__ next) {
-  using S = QcShapeH2<G, Z, R, SPLIT>;
-  static_assert(S::CHN_SMEM, "the persistent decoder refills the cached channel LLRs per slot");
+// iteration semantics as k_qc_fast_h2 (the halves never interact).  Needs the
+// channel LLRs cached in shared memory (the launcher checks).
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT_MAX, 1)
+    k_qc_fast_h2p(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
+                  float alpha, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
+                  int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
+                  unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next) {
+  constexpr int SPLIT = Geo::SPLIT;
   extern __shared__ uint32_t smw[];
+  const int NV = geo.nv(), NT = geo.nt();
   uint32_t *tot = smw;
-  uint32_t *chn = smw + SPLIT * S::NV;
-  __shared__ unsigned red[S::NT / 32];
+  uint32_t *chn = smw + SPLIT * NV;
+  __shared__ unsigned red[Geo::NT_MAX / 32];
   __shared__ long long slot_cw[2];
   __shared__ int slot_it[2], slot_new[2];
   const int t = threadIdx.x;
-  const int h = t / S::NT1;
-  const int i = t - h * S::NT1;
-  const bool lane = i < Z;
+  const int h = t / geo.nt1();
+  const int i = t - h * geo.nt1();
+  const bool lane = i < geo.z();
   char *const base = reinterpret_cast<char *>(smw);
   const __half2 al2 = __float2half2_rn(alpha);
   const bool scaled = alpha != 1.0f;
-  H2State<S::NR> st;
+  H2State<Geo::NR> st;
 #pragma unroll
-  for (int j = 0; j < S::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+  for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
   if (t == 0) {
     slot_cw[0] = slot_cw[1] = -1;
     slot_it[0] = slot_it[1] = 0;
   }
   __syncthreads();
-  auto chan_word = [&](int v) { return chn[v]; };  // unused: CHN_SMEM
+  auto chan_word = [&](int v) { return chn[v]; };  // channel words are always cached here
   for (;;) {
     // ---- refill empty slots
     if (t == 0) {
@@ -428,18 +483,18 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
       for (int q = 0; q < 2; ++q) {
         if (!(q ? new1 : new0)) continue;
         const float *row = llr + (q ? cw1 : cw0) * (int64_t)P.n;
-        for (int v = t; v < S::NV; v += S::NT) {
+        for (int v = t; v < NV; v += NT) {
           const unsigned short hv = __half_as_ushort(__float2half_rn(chan_value(P, row, v)));
           c16[2 * v + q] = hv;
           t16[2 * v + q] = hv;
         }
       }
       // fresh check state for the refilled half (the other half continues)
-      h2_reset_half<G, Z, R, SPLIT>(st, h, new0, new1);
+      h2_reset_half<Geo>(st, h, new0, new1);
       __syncthreads();
     }
     // ---- one iteration for both slots
-    const uint32_t synx = h2_cn<G, Z, R, SPLIT>(st, base, h, lane, al2, scaled);
+    const uint32_t synx = h2_cn(st, base, h, lane, al2, scaled, geo);
     const int bad0 = __syncthreads_or(lane && ((synx >> 15) & 1u));
     const int bad1 = __syncthreads_or(lane && (synx >> 31));
     bool freed = false;
@@ -449,8 +504,8 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
       const int itq = slot_it[q];
       const bool conv = itq > 0 && !(q ? bad1 : bad0);
       if (conv || itq == num_iter) {
-        h2_emit<S::NT>(P, tot, S::NV, cw, llr + cw * (int64_t)P.n, q, itq, hard_k, llr_out, iters_used, ref,
-                       counts, red);
+        h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cw, llr + cw * (int64_t)P.n, q, itq, hard_k, llr_out, iters_used, ref,
+                             counts, red);
         __syncthreads();
         if (t == 0) slot_cw[q] = -1;
         freed = true;
@@ -460,7 +515,7 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
       __syncthreads();
       if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
     }
-    h2_vn<G, Z, R, SPLIT>(st, tot, chn, base, h, lane, t, chan_word);
+    h2_vn(st, tot, chn, base, h, lane, t, chan_word, geo);
     if (t == 0) {
       slot_it[0] += 1;
       slot_it[1] += 1;
@@ -468,46 +523,87 @@ __global__ void __launch_bounds__(QcShapeH2<G, Z, R, SPLIT>::NT, 1)
   }
 }
 
-template <class G, int Z, int R, int SPLIT>
-int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
-                      uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
-                      unsigned long long *counts, cudaStream_t s) {
-  using S = QcShapeH2<G, Z, R, SPLIT>;
+// launch either kernel for a geometry with `nt` threads and `smem` bytes of
+// dynamic shared memory; the persistent one when early stopping and the
+// channel LLRs fit in shared memory
+template <class Geo>
+int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanParams &P, const float *llr, int64_t B,
+              int num_iter, float alpha, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,
+              const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
   cudaError_t e;
-  if constexpr (S::CHN_SMEM) {
-    if (early_stop && B >= 4) {  // persistent slot-refilling decoder
-      auto kp = k_qc_fast_h2p<G, Z, R, SPLIT>;
-      e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
-      int dev = 0, sms = 148, per_sm = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, S::NT, S::SMEM);
-      const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
-      unsigned long long *next = nullptr;
-      e = cudaMallocAsync((void **)&next, sizeof(unsigned long long), s);
-      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(counter)");
-      cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
-      kp<<<(unsigned)grid, S::NT, S::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, llr_out, iters_used, ref, counts,
-                                                next);
-      e = cudaGetLastError();
-      cudaFreeAsync(next, s);
-      return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
-    }
+  if (chn_smem && early_stop && B >= 4) {  // persistent slot-refilling decoder
+    auto kp = k_qc_fast_h2p<Geo>;
+    e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, nt, smem);
+    const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
+    unsigned long long *next = nullptr;
+    e = cudaMallocAsync((void **)&next, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(counter)");
+    cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+    kp<<<(unsigned)grid, nt, smem, s>>>(P, geo, llr, B, num_iter, alpha, hard_k, llr_out, iters_used, ref, counts,
+                                        next);
+    e = cudaGetLastError();
+    cudaFreeAsync(next, s);
+    return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
   }
-  auto kern = k_qc_fast_h2<G, Z, R, SPLIT>;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+  auto kern = k_qc_fast_h2<Geo>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   const int64_t chunk = 2LL * 0x3fffffff;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t nb = B - b0 < chunk ? B - b0 : chunk;
-    kern<<<(unsigned)((nb + 1) / 2), S::NT, S::SMEM, s>>>(
-        P, llr + b0 * P.n, nb, num_iter, alpha, early_stop, hard_k ? hard_k + b0 * P.k : nullptr,
+    kern<<<(unsigned)((nb + 1) / 2), nt, smem, s>>>(
+        P, geo, llr + b0 * P.n, nb, num_iter, alpha, early_stop, hard_k ? hard_k + b0 * P.k : nullptr,
         llr_out ? llr_out + b0 * P.n_full : nullptr, iters_used ? iters_used + b0 : nullptr,
         ref ? ref + b0 * P.k : nullptr, counts);
   }
   e = cudaGetLastError();
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+}
+
+// specialised instance (qc_instances.h)
+template <class G, int Z, int R, int SPLIT>
+int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
+                      uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
+                      unsigned long long *counts, cudaStream_t s) {
+  using S = QcShapeH2<G, Z, R, SPLIT>;
+  return launch_h2(H2GeoCT<G, Z, R, SPLIT>{}, S::NT, S::SMEM, S::CHN_SMEM, P, llr, B, num_iter, alpha, early_stop,
+                   hard_k, llr_out, iters_used, ref, counts, s);
+}
+
+// runtime-geometry instance: any Z <= 384 (<= 192 when SPLIT = 4) and any
+// processed-row count R <= RB; `s_mod_z` are the code's shifts mod Z and
+// `col` the base-graph columns, in entry order
+template <class G, int RB, int SPLIT>
+int launch_qc_h2rt(const QcChanParams &P, int R, const uint16_t *s_mod_z, const int32_t *col, const float *llr,
+                   int64_t B, int num_iter, float alpha, int early_stop, uint8_t *hard_k, float *llr_out,
+                   int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
+  using Geo = H2GeoRT<G, RB, SPLIT>;
+  static_assert(sizeof(Geo) + sizeof(QcChanParams) + 96 <= 4096, "kernel parameters too large");
+  const int Z = P.z;
+  if (R < 1 || R > RB) return fail(LS_EINVAL, "ls_qc_decode: row count outside the runtime-geometry instance");
+  Geo geo;
+  geo.Z = Z;
+  geo.NT1 = ((Z + 31) / 32) * 32;
+  geo.NT = geo.NT1 * SPLIT;
+  if (geo.NT > Geo::NT_MAX) return fail(LS_EINVAL, "ls_qc_decode: lifting size too large for this instance");
+  geo.R = R;
+  geo.NV = (G::KB + (R > 4 ? R : 4)) * Z;
+  geo.Z4 = 4u * (unsigned)Z;
+  const size_t arr = 4 * (size_t)geo.NV;
+  geo.CHN = (SPLIT + 1) * arr <= 225 * 1024;
+  const size_t smem = (SPLIT + (geo.CHN ? 1 : 0)) * arr;
+  if (smem > 227 * 1024) return fail(LS_EINVAL, "ls_qc_decode: code too large for the fp16x2 decoder");
+  for (int e = 0; e < Geo::NE; ++e) {
+    geo.s4[e] = 4u * s_mod_z[e];
+    geo.cb[e] = 4u * (unsigned)Z * (unsigned)col[e];
+  }
+  return launch_h2(geo, geo.NT, smem, geo.CHN != 0, P, llr, B, num_iter, alpha, early_stop, hard_k, llr_out,
+                   iters_used, ref, counts, s);
 }
 
 }  // namespace lsb

@@ -648,6 +648,9 @@ int ls_code_create(int bg, int z, int k, int n, int mb, int nb, int kb, const in
     c->entries[3 * e + 2] = s;
     P.s[e] = (uint16_t)(((s % z) + z) % z);
   }
+  const int *wshift = bg == 1 ? BG1Tables::shift : BG2Tables::shift;
+  c->std_shifts = 1;
+  for (int e = 0; e < nnz; ++e) c->std_shifts &= (entries[3 * e + 2] == wshift[e]);
   *out = c;
   return LS_OK;
 }

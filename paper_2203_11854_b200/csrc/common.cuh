@@ -55,6 +55,7 @@ struct QcParams {
 struct ls_code {
   lsb::QcParams p;
   int32_t entries[3 * lsb::kMaxNnz];
+  int std_shifts;  // shifts equal the compiled base-graph tables (specialised kernels usable)
 };
 
 struct ls_graph {

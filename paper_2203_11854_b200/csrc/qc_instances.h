@@ -1,7 +1,8 @@
 // Specialised fast-decoder instances compiled in: (base graph, Z, processed
 // rows, threads per lane, kind).  Each becomes build/gen/qc_<...>.cu.
-// Min-sum codes matching none of them use the runtime-Z fp32 kernel in
-// bp_fast.cu; sum-product fast mode exists only for these instances.
+// fp16x2 min-sum codes matching none of them use a runtime-geometry instance
+// (LSB_QC_RT_INSTANCES below); fp32 ones the runtime-Z kernel in bp_fast.cu;
+// sum-product fast mode exists only for these instances.
 //   1,384,24 / 1,384,46 : config 2 (k=8448 n=16896), dead rows pruned / all
 //   1,192,{24,45,46}    : configs 3 and 4 (k=4096, n=8192 / 12288)
 //   2,26,{12,42}        : config 1 (k=256 n=512)
@@ -41,3 +42,16 @@
   X(1, 192, 46, 2, sp)      \
   X(2, 26, 12, 1, sp)       \
   X(2, 26, 42, 1, sp)
+
+// Runtime-geometry fp16x2 instances (base graph, row bound RB, threads per
+// lane): any Z <= 384 (<= 192 with 4 threads per lane) and any processed-row
+// count R <= RB.  The dispatcher picks the smallest RB >= R that fits.
+#define LSB_QC_RT_INSTANCES(Y) \
+  Y(1, 12, 2)                  \
+  Y(1, 24, 2)                  \
+  Y(1, 46, 2)                  \
+  Y(1, 46, 4)                  \
+  Y(2, 12, 2)                  \
+  Y(2, 22, 2)                  \
+  Y(2, 42, 2)                  \
+  Y(2, 42, 4)

@@ -209,7 +209,7 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
     if mode != "fast":
         raise ValueError(f"unknown decoder mode {mode!r}")
     if precision == "auto":
-        precision = "fp16x2" if qc_has_kernel(code, "fp16x2", prune=True) else "fp32"
+        precision = "fp16x2"  # specialised instance, else the runtime-geometry fp16x2 kernel
     host_in = not L.is_tensor(llr) or not llr.is_cuda
     if host_in and not device:
         return _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, precision)
@@ -255,7 +255,8 @@ LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP = 1, 2, 4, 8
 def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
                   variant: str = "min-sum") -> bool:
     """Whether a compile-time specialised fast decoder exists for this code
-    (the sum-product fast decoder exists only as such instances)."""
+    (the sum-product fast decoder exists only as such instances; min-sum codes
+    without one run the runtime-geometry fp16x2 or the runtime-Z fp32 kernel)."""
     flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
     if variant == "sum-product":
         flags |= LS_QC_SP
@@ -272,7 +273,9 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
 
     prune (default: on unless mother LLRs are requested) skips the dead
     extension rows whose parity bit is never transmitted.  precision
-    "fp16x2" selects the packed two-codewords-per-lane kernel."""
+    "fp16x2" selects the packed two-codewords-per-lane kernel.  generic forces
+    the runtime-geometry kernel of that precision instead of a compile-time
+    specialised instance."""
     if prune is None:
         prune = not want_llr
     if precision not in ("fp32", "fp16x2"):

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 from . import _lib as L
 from .channel import awgn
 from .core import RngStream, binary_source, ebnodb2no
-from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode, qc_has_kernel
+from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode
 from .mapping import Constellation, demap_app, demap_maxlog, map_bits, modem_qam
 
 CSV_COLUMNS = ("ebno_db", "bits", "bit_errors", "ber", "blocks", "block_errors", "bler", "batches",
@@ -231,7 +231,7 @@ class Pipeline:
     def precision(self) -> str:
         if self.decoder_precision != "auto":
             return self.decoder_precision
-        return "fp16x2" if qc_has_kernel(self.ldpc, "fp16x2", prune=True) else "fp32"
+        return "fp16x2"
 
     def run_batch_device(self, ebno_db: float, batch_size: int, rng: RngStream, lo: int = 0):
         """(payload, decoded) as CUDA tensors (rows [lo, lo + batch_size))."""

@@ -379,6 +379,66 @@ def test_fast_decoder_noiseless_round_trip_and_early_stop():
                     assert np.array_equal(it, it_ref)
 
 
+@pytest.mark.parametrize("k,n,m,ebno", [(792, 1584, 2, 3.0), (3520, 5280, 4, 6.5), (1144, 3432, 2, 3.0),
+                                        (200, 600, 2, 3.5), (7040, 10560, 4, 7.0), (120, 240, 2, 4.0)])
+@pytest.mark.parametrize("es", [True, False])
+def test_fp16x2_runtime_geometry_decoder(k, n, m, ebno, es):
+    """Lifting sizes / rates with no specialised instance (Z = 36, 160, 52,
+    20, 320, 12) run the runtime-geometry fp16x2 kernel: converged blocks
+    identical to the reference, block errors statistically equal."""
+    code = lb.LdpcCode5G(k, n)
+    assert not lb.ldpc.qc_has_kernel(code, "fp16x2")
+    B = 41 if k < 3000 else 13
+    bits, llr = _oracle_llrs(k, n, m, ebno, B, 21)
+    res = lb.qc_decode(llr, code, 20, "min-sum", early_stop=es, ref_bits=bits, want_iters=True, precision="fp16x2")
+    hard = res["hard"].cpu().numpy()
+    ref_hard, _, it_o = O.decode(llr, O.code(k, n), 20, "min-sum", 0.75, True)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    ok_fast = (hard == bits).all(axis=1)
+    # blocks the reference converges on with iterations to spare (a block it
+    # only just converges on at iteration 19 may need one more in fp16)
+    conv = (it_o <= 16) & ok_ref
+    assert conv.sum() >= B // 4
+    assert np.array_equal(hard[conv], ref_hard[conv])
+    assert (ok_ref != ok_fast).sum() <= max(1, B // 12)
+    cnt = res["counts"].cpu().numpy()
+    assert cnt[0] == int((hard != bits).sum()) and cnt[1] == int((~ok_fast).sum())
+    it = res["iters"].cpu().numpy()
+    assert (it == 20).all() if not es else ((it >= 1).all() and (it <= 20).all())
+
+
+def test_fp16x2_runtime_geometry_equals_specialised_instance():
+    """Where the runtime-geometry kernel runs the same thread layout as a
+    specialised instance (config 2, 2 threads per lane), the two compute the
+    same arithmetic in the same order: bit-identical outputs."""
+    k, n = 8448, 16896
+    bits, llr = _oracle_llrs(k, n, 4, 5.8, 12, 4)
+    code = lb.LdpcCode5G(k, n)
+    for prune in (True, False):
+        assert lb.ldpc.qc_has_kernel(code, "fp16x2", prune=prune)
+        for es in (True, False):
+            kw = dict(early_stop=es, want_llr=True, want_iters=True, prune=prune, precision="fp16x2")
+            a = lb.qc_decode(llr, code, 20, "scaled-min-sum", **kw)
+            g = lb.qc_decode(llr, code, 20, "scaled-min-sum", generic=True, **kw)
+            for key in ("hard", "llr", "iters"):
+                assert torch.equal(a[key], g[key]), (prune, es, key)
+
+
+def test_fp16x2_noiseless_round_trip_any_lifting_size():
+    # (rate-0.8 codes of the synthetic graph do not recover their punctured
+    # columns even noiselessly, in the reference too, so none are listed)
+    for k, n in [(20, 60), (40, 100), (100, 300), (500, 1000), (2000, 3000), (6000, 18000), (8448, 25344)]:
+        code = lb.LdpcCode5G(k, n)
+        bits = lb.binary_source([9, k], lb.RngStream(k))
+        tx = lb.ldpc5g_encode(bits, code)
+        llr = ((2.0 * tx - 1.0) * 8.0).astype(np.float32)
+        for generic in (False, True):
+            res = lb.qc_decode(llr, code, 10, "min-sum", early_stop=True, want_iters=True, precision="fp16x2",
+                               generic=generic)
+            assert np.array_equal(res["hard"].cpu().numpy(), bits), (k, n, generic)
+            assert (res["iters"].cpu().numpy() <= 3).all()
+
+
 @pytest.mark.parametrize("k,n,m,ebno", [(8448, 16896, 4, 5.8), (4096, 8192, 2, 3.0), (4096, 12288, 6, 7.0),
                                         (256, 512, 2, 3.5)])
 def test_specialised_decoder_equals_generic_kernel(k, n, m, ebno):
