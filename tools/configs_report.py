@@ -85,8 +85,12 @@ def config4(quick):
 
 
 def config5(quick):
+    """Decoder-only table: every lifting size in [32, 384],
+    BG1 rate 1/2 and BG2 rate 1/3, 5-50 fixed iterations, min-sum and scaled
+    min-sum on the fp16x2 decoder (specialised instance where compiled, else
+    the runtime-geometry kernel) and sum-product where an instance exists."""
     iters = [5, 10, 20, 50]
-    zs = [32, 64, 96, 128, 192, 256, 384] if not quick else [96, 384]  # 96: runtime-Z kernel
+    zs = [z for z in lb.ldpc.LIFTING_SIZES if 32 <= z <= 384] if not quick else [96, 384]
     rows = []
     for bg in (1, 2):
         kb = 22 if bg == 1 else 10
@@ -95,13 +99,17 @@ def config5(quick):
             n = 2 * k if bg == 1 else 3 * k
             code = lb.LdpcCode5G(k, n, base_graph=bg, z=z)
             B = max(256, min(65536, (1 << 26) // (68 * z)))
+            B += B & 1
             torch.manual_seed(0)
             llr = (torch.randn(B, n, device="cuda") * 2.0 + 3.0).contiguous()  # all-zero codeword, ~4 dB
-            for variant in ("min-sum", "sum-product"):
+            edges = code.pcm.num_edges
+            live = int(lb._lib.lib().ls_qc_live_rows(code.handle))
+            for variant in ("min-sum", "scaled-min-sum", "sum-product"):
                 if variant == "sum-product" and not lb.ldpc.qc_has_kernel(code, variant=variant):
                     rows.append({"bg": bg, "z": z, "variant": variant, "note": "no sum-product instance"})
                     continue
-                prec = "fp16x2" if (variant == "min-sum" and lb.ldpc.qc_has_kernel(code, "fp16x2")) else "fp32"
+                prec = "fp32" if variant == "sum-product" else "fp16x2"
+                spec = lb.ldpc.qc_has_kernel(code, prec, variant=variant)
                 for it in iters:
                     lb.qc_decode(llr, code, it, variant, early_stop=False, want_hard=True, precision=prec)
                     torch.cuda.synchronize()
@@ -111,13 +119,12 @@ def config5(quick):
                     e1.record()
                     torch.cuda.synchronize()
                     ms = e0.elapsed_time(e1)
+                    kind = ("specialised " if spec else "runtime-geometry ") + (
+                        "sum-product fp16" if variant == "sum-product" else "fp16x2")
                     rows.append({"bg": bg, "z": z, "k": k, "n": n, "variant": variant, "iters": it,
-                                 "kernel": ("specialised " + prec) if lb.ldpc.qc_has_kernel(code, prec) or
-                                 variant == "sum-product" else "runtime-Z fp32",
-                                 "batch": B, "ms": ms, "info_gbit_s": B * k / ms / 1e6,
-                                 "live_rows": int(lb._lib.lib().ls_qc_live_rows(code.handle)),
-                                 "mother_graph_edge_updates_per_s":
-                                     B * it * code.pcm.num_edges / (ms / 1e3)})
+                                 "kernel": kind, "batch": B, "ms": ms, "info_gbit_s": B * k / ms / 1e6,
+                                 "live_rows": live,
+                                 "mother_graph_edge_updates_per_s": B * it * edges / (ms / 1e3)})
     return rows
 
 
@@ -128,7 +135,11 @@ def main():
     p.add_argument("--only", default="3,4,5")
     a = p.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
-    rep = {"device": torch.cuda.get_device_name(0)}
+    rep = {}
+    if os.path.exists(a.out):  # refresh only the configs asked for
+        with open(a.out) as f:
+            rep = json.load(f)
+    rep["device"] = torch.cuda.get_device_name(0)
     if "3" in a.only:
         rep["config3_sweep"] = config3(a.quick, os.path.dirname(os.path.abspath(a.out)))
     if "4" in a.only:
