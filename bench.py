@@ -144,6 +144,11 @@ class Clocks:
 
     def __exit__(self, *exc):
         if self.proc:
+            # a timed region shorter than the 100 ms sampling period still
+            # gets one sample (taken right after it)
+            t_end = time.perf_counter() + 1.0
+            while not self.samples and time.perf_counter() < t_end:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -168,12 +173,20 @@ def run_b200(a, rank, world, local_rank):
     import paper_2203_11854_b200 as lb
     from paper_2203_11854_b200 import _lib as L
 
+    # LS_BENCH_BACKEND=gloo only exists to exercise the multi-rank code path
+    # on a single-GPU box (ranks then share the device; timings meaningless)
+    backend = os.environ.get("LS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     cfg = lb.SimConfig.from_dict({
         "code": {"family": "ldpc5g", "k": K_INFO, "n": N_TX,
                  "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "fast",
