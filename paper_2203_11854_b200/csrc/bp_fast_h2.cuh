@@ -76,6 +76,8 @@ struct H2GeoCT {
   __device__ __forceinline__ static constexpr int nv() { return S::NV; }
   __device__ __forceinline__ static constexpr bool chn_smem() { return S::CHN_SMEM; }
   __device__ __forceinline__ static constexpr int z() { return Z; }
+  // every thread of a slot serves a lane (Z a multiple of 32)
+  __device__ __forceinline__ static constexpr bool full_lanes() { return S::NT1 == Z; }
   template <int r>
   __device__ __forceinline__ static constexpr bool live() { return true; }
   template <int e>
@@ -97,6 +99,7 @@ struct H2GeoRT {
   __device__ __forceinline__ int nv() const { return NV; }
   __device__ __forceinline__ bool chn_smem() const { return CHN != 0; }
   __device__ __forceinline__ int z() const { return Z; }
+  __device__ __forceinline__ static constexpr bool full_lanes() { return false; }
   template <int r>
   __device__ __forceinline__ bool live() const { return r < R; }
   template <int e>
@@ -265,18 +268,21 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
     }
   }
   __syncthreads();
-  sfor<0, NR>([&](auto jc) {
-    constexpr int j = decltype(jc)::value;
-    if (lane) {
-      sfor<0, SPLIT>([&](auto hc) {
-        constexpr int H = decltype(hc)::value;
-        constexpr int r = j * SPLIT + H;
-        if constexpr (r < Geo::RB) {
-          if (h != H || !geo.template live<r>()) return;
+  // slot H accumulates its rows into its own array, one row per barrier step
+  // (consecutive rows of a slot may share variables); every slot passes the
+  // same NR barriers, so the slot branch is taken once per phase
+  sfor<0, SPLIT>([&](auto hc) {
+    constexpr int H = decltype(hc)::value;
+    if (h != H) return;
+    const unsigned i4 = 4u * tid_volatile() - 4u * H * geo.nt1();
+    char *const arr = base + 4u * H * NV;
+    sfor<0, NR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      constexpr int r = j * SPLIT + H;
+      if constexpr (r < Geo::RB) {
+        if (lane && geo.template live<r>()) {
           constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
           constexpr bool packed = d <= 16;
-          const unsigned i4 = 4u * tid_volatile() - 4u * H * geo.nt1();
-          char *const arr = base + 4u * H * NV;
           const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
           const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
           sfor<e0, e1>([&](auto ec) {
@@ -294,9 +300,9 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
             *tp = h2u(__hadd2(u2h(*tp), u2h(mag | sgn)));
           });
         }
-      });
-    }
-    __syncthreads();
+      }
+      __syncthreads();
+    });
   });
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
   if (NV % 4 == 0) {
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
   const int t = threadIdx.x;
   const int h = t / geo.nt1();
   const int i = t - h * geo.nt1();
-  const bool lane = i < geo.z();
+  const bool lane = geo.full_lanes() || i < geo.z();
   char *const base = reinterpret_cast<char *>(smw);
   const int64_t cwA = 2 * (int64_t)blockIdx.x, cwB = cwA + 1;
   const bool hasB = cwB < batch;
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   const int t = threadIdx.x;
   const int h = t / geo.nt1();
   const int i = t - h * geo.nt1();
-  const bool lane = i < geo.z();
+  const bool lane = geo.full_lanes() || i < geo.z();
   char *const base = reinterpret_cast<char *>(smw);
   const __half2 al2 = __float2half2_rn(alpha);
   const bool scaled = alpha != 1.0f;
