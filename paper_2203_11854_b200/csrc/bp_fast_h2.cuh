@@ -182,12 +182,11 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         if (!geo.template live<r>()) return;
         constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
         constexpr bool packed = d <= 16;
-        // ALU-pipe relief: the min1/min2 select and the argmin update are
-        // fp16 FMAs on 1.0/0.0 compare results (FMA pipe)
+        // ALU-pipe relief: the min1/min2 select is an fp16 FMA on a 1.0/0.0
+        // compare result (FMA pipe)
         const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
         const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
-        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u;
-        __half2 nix = u2h(0u);
+        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u, nix = 0u;
         sfor<e0, e1>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int p = e - e0;
@@ -205,7 +204,9 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
-          nix = __hfma2(__hlt2(a, u2h(n1)), __hsub2(pp, nix), nix);
+          // argmin: per-half mask select (HSET2 + LOP3); first minimum wins
+          const uint32_t lt = __hlt2_mask(a, u2h(n1));
+          nix = (lt & h2_int<p>()) | (~lt & nix);
           n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
           n1 = h2u(__hmin2(u2h(n1), a));
           if constexpr (packed) {
@@ -235,7 +236,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         // edge is reconstructed as min1 + diff (within 1 ulp of min2)
         st.M1[j] = n1;
         st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
-        st.IX[j] = h2u(nix);
+        st.IX[j] = nix;
         synx |= hs;
       }
     });
