@@ -327,76 +327,11 @@ __global__ void k_demap_qam(const float2 *__restrict__ y, int64_t nsym, double n
   }
 }
 
-// ------------------------------------------------------------ encoder
-// One CTA per codeword, thread i = circulant lane.  Row syndromes of the
-// systematic part (ldpc.py:308-311, as XORs instead of the GEMM), the
-// accumulate-core solve (ldpc.py:313-320), the extension rows
-// (ldpc.py:327-331), then the rate-matching gather (ldpc.py:351).
-template <class G>
-__global__ void k_encode(QcParams P, const uint8_t *__restrict__ bits, uint8_t *__restrict__ tx,
-                         uint8_t *__restrict__ full) {
-  extern __shared__ uint8_t sm[];
-  const int Z = P.z;
-  uint8_t *cw = sm;                 // [n_full] mother codeword
-  uint8_t *syn = sm + P.n_full;     // [mb * Z]
-  const int64_t b = blockIdx.x;
-  const uint8_t *in = bits + b * (int64_t)P.k;
-  for (int v = threadIdx.x; v < P.k_full; v += blockDim.x) cw[v] = v < P.k ? (in[v] & 1) : 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
-    for (int r = 0; r < G::MB; ++r) {
-      uint8_t acc = 0;
-      for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
-        const int c = G::d_col(e);
-        if (c < G::KB) {
-          int t = i + P.s[e];
-          t = t >= Z ? t - Z : t;
-          acc ^= cw[c * Z + t];
-        }
-      }
-      syn[r * Z + i] = acc;
-    }
-  }
-  __syncthreads();
-  uint8_t *core = cw + P.k_full;  // p1..p4 blocks
-  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
-    const int im1 = i == 0 ? Z - 1 : i - 1;
-    const uint8_t ss_im1 = syn[im1] ^ syn[Z + im1] ^ syn[2 * Z + im1] ^ syn[3 * Z + im1];
-    const uint8_t ss = syn[i] ^ syn[Z + i] ^ syn[2 * Z + i] ^ syn[3 * Z + i];
-    const uint8_t p1 = ss_im1, p2 = syn[i] ^ ss, p3 = syn[Z + i] ^ p1 ^ p2, p4 = syn[2 * Z + i] ^ p3;
-    core[i] = p1;
-    core[Z + i] = p2;
-    core[2 * Z + i] = p3;
-    core[3 * Z + i] = p4;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < Z; i += blockDim.x) {
-    for (int r = 4; r < G::MB; ++r) {
-      uint8_t acc = syn[r * Z + i];
-      for (int e = G::d_row_start(r); e < G::d_row_start(r + 1); ++e) {
-        const int c = G::d_col(e);
-        if (c >= G::KB && c < G::KB + 4) {
-          int t = i + P.s[e];
-          t = t >= Z ? t - Z : t;
-          acc ^= core[(c - G::KB) * Z + t];
-        }
-      }
-      cw[P.k_full + r * Z + i] = acc;
-    }
-  }
-  __syncthreads();
-  if (full) {
-    uint8_t *o = full + b * (int64_t)P.n_full;
-    for (int v = threadIdx.x; v < P.n_full; v += blockDim.x) o[v] = cw[v];
-  }
-  if (tx) {
-    uint8_t *o = tx + b * (int64_t)P.n;
-    for (int j = threadIdx.x; j < P.n; j += blockDim.x) o[j] = cw[mother_of(P, j)];
-  }
-}
-
 // ------------------------------------------------------------ bit-packed encoder
-// Same algebra as k_encode, 32 circulant lanes per 32-bit word: a circulant
+// Row syndromes of the systematic part (ldpc.py:308-311, as XORs instead of
+// the GEMM), the accumulate-core solve (ldpc.py:313-320), the extension rows
+// (ldpc.py:327-331), then the rate-matching gather (ldpc.py:351), with 32
+// circulant lanes per 32-bit word: a circulant
 // with shift s maps word w of the output to the 32 input bits starting at
 // bit 32w + s of a "doubled" copy of the input vector (bit j = x[j mod Z]),
 // i.e. one funnel shift per (row, word, entry).  One CTA per codeword.
