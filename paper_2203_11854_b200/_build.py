@@ -56,6 +56,15 @@ def _instance_sources():
                 f"  return launch_qc_h2rt<BG{bg}Tables, {rb}, {sp}>(P, R, s, col, l, B, it, a, es, h, lo, iu, ref, cnt, st);\n"
                 "}\n}  // namespace lsb\n")
         out.append(_write(f"qcrt_{bg}_{rb}_{sp}.cu", body))
+    for bg, rb, sp in re.findall(r"W\((\d+),\s*(\d+),\s*(\d+)\)", text):
+        body = (f'#include "{CSRC}/bp_fast_sp.cuh"\n'
+                "namespace lsb {\n"
+                f"int qcsprt_{bg}_{rb}_{sp}(const QcChanParams &P, int R, const uint16_t *s, const int32_t *col,\n"
+                "    const float *l, int64_t B, int it, float a, int es, uint8_t *h, float *lo, int32_t *iu,\n"
+                "    const uint8_t *ref, unsigned long long *cnt, cudaStream_t st) {\n"
+                f"  return launch_qc_sprt<BG{bg}Tables, {rb}, {sp}>(P, R, s, col, l, B, it, a, es, h, lo, iu, ref, cnt, st);\n"
+                "}\n}  // namespace lsb\n")
+        out.append(_write(f"qcsprt_{bg}_{rb}_{sp}.cu", body))
     return out
 
 

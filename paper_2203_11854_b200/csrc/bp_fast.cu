@@ -238,12 +238,21 @@ struct QcRtEntry {
 #define LSB_QC_RT_ENTRY(bg, rb, sp) {bg, rb, sp, &qcrt_##bg##_##rb##_##sp},
 static const QcRtEntry kQcRtKernels[] = {LSB_QC_RT_INSTANCES(LSB_QC_RT_ENTRY)};
 
+#define LSB_QC_SPRT_DECL(bg, rb, sp)                                                                           \
+  int qcsprt_##bg##_##rb##_##sp(const QcChanParams &, int, const uint16_t *, const int32_t *, const float *, \
+                                int64_t, int, float, int, uint8_t *, float *, int32_t *, const uint8_t *,    \
+                                unsigned long long *, cudaStream_t);
+LSB_QC_SPRT_INSTANCES(LSB_QC_SPRT_DECL)
+#define LSB_QC_SPRT_ENTRY(bg, rb, sp) {bg, rb, sp, &qcsprt_##bg##_##rb##_##sp},
+static const QcRtEntry kQcSpRtKernels[] = {LSB_QC_SPRT_INSTANCES(LSB_QC_SPRT_ENTRY)};
+
 // runtime-geometry fp16x2 instance for (BG, Z, R): smallest row bound >= R,
 // then the most threads per lane that fit 768 threads
-static const QcRtEntry *pick_rt(int bg, int z, int R) {
+template <size_t N>
+static const QcRtEntry *pick_rt(const QcRtEntry (&table)[N], int bg, int z, int R) {
   const QcRtEntry *best = nullptr;
   const int nt1 = ((z + 31) / 32) * 32;
-  for (const QcRtEntry &k : kQcRtKernels) {
+  for (const QcRtEntry &k : table) {
     if (k.bg != bg || k.rb < R || nt1 * k.split > 768) continue;
     if (!best || k.rb < best->rb || (k.rb == best->rb && k.split > best->split)) best = &k;
   }
@@ -290,8 +299,6 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
   const int prec = qc_kind(variant, flags);
-  if (prec == 2 && (flags & LS_QC_GENERIC))
-    return fail(LS_EINVAL, "ls_qc_decode: the sum-product fast decoder has no runtime-Z kernel");
   const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;
   const QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
   if (!(flags & LS_QC_GENERIC) && code->std_shifts) {
@@ -300,12 +307,12 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
         return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
     }
   }
-  if (prec == 2)
-    return fail(LS_EINVAL, "ls_qc_decode: no sum-product fast decoder instance for this (BG, Z, rows); "
-                           "use the exact decoder");
-  if (prec == 1) {  // fp16x2 at any (Z, R): runtime-geometry instance
-    const QcRtEntry *k = pick_rt(P.bg, P.z, R);
-    if (!k) return fail(LS_EINVAL, "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)");
+  if (prec >= 1) {  // fp16x2 / sum-product at any (Z, R): runtime-geometry instance
+    const QcRtEntry *k = prec == 1 ? pick_rt(kQcRtKernels, P.bg, P.z, R) : pick_rt(kQcSpRtKernels, P.bg, P.z, R);
+    if (!k)
+      return fail(LS_EINVAL, prec == 1 ? "ls_qc_decode: no fp16x2 decoder instance for this (BG, Z, rows)"
+                                       : "ls_qc_decode: no sum-product fast decoder instance for this (BG, Z, rows); "
+                                         "use the exact decoder");
     int32_t col[kMaxNnz];
     for (int e = 0; e < P.nnz; ++e) col[e] = code->entries[3 * e + 1];
     return k->fn(CP, R, P.s, col, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits,

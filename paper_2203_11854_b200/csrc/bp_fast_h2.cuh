@@ -590,7 +590,7 @@ int launch_qc_h2rt(const QcChanParams &P, int R, const uint16_t *s_mod_z, const 
                    int64_t B, int num_iter, float alpha, int early_stop, uint8_t *hard_k, float *llr_out,
                    int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
   using Geo = H2GeoRT<G, RB, SPLIT>;
-  static_assert(sizeof(Geo) + sizeof(QcChanParams) + 96 <= 4096, "kernel parameters too large");
+  static_assert(sizeof(Geo) + sizeof(QcChanParams) + 96 <= 32000, "kernel parameters too large");  // CUDA >= 12.1
   const int Z = P.z;
   if (R < 1 || R > RB) return fail(LS_EINVAL, "ls_qc_decode: row count outside the runtime-geometry instance");
   Geo geo;

@@ -53,25 +53,91 @@ __device__ __forceinline__ unsigned vn_off2(unsigned i2) {  // byte offset of (c
   return CB + min(i2 + S2, i2 + (S2 - 2u * (unsigned)Z));
 }
 
-template <class G, int Z, int R, int SPLIT>
-__global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z, R, SPLIT>::MINB)
-    k_qc_sp(const QcChanParams P, const float *__restrict__ llr, int num_iter, int early_stop,
+// Geometry policies (as for the fp16x2 min-sum decoder): everything
+// compile-time for the specialised instances, or Z / processed rows R <= RB
+// runtime with the per-edge offsets in the kernel's parameter space.
+template <class G_, int Z, int R, int SPLIT_>
+struct SpGeoCT {
+  using G = G_;
+  using S = QcShapeSP<G_, Z, R, SPLIT_>;
+  static constexpr int SPLIT = SPLIT_, RB = R, NT_MAX = S::NT, MINB = S::MINB;
+  static constexpr int NCOL_MAX = S::NCOL;
+  __device__ __forceinline__ static constexpr int z() { return Z; }
+  __device__ __forceinline__ static constexpr int nt1() { return S::NT1; }
+  __device__ __forceinline__ static constexpr int nt() { return S::NT; }
+  __device__ __forceinline__ static constexpr int ne() { return S::NE; }
+  __device__ __forceinline__ static constexpr int ncol() { return S::NCOL; }
+  __device__ __forceinline__ static constexpr bool full_lanes() { return S::NT1 == Z; }
+  template <int r>
+  __device__ __forceinline__ static constexpr bool live() { return true; }
+  // byte offset of posterior (c, (i + s) mod Z) for lane byte offset i2
+  template <int e>
+  __device__ __forceinline__ static unsigned off(unsigned i2) { return vn_off2<G_, Z, e>(i2); }
+  // element offset of message (e, (j - s) mod Z) for lane j
+  template <int e>
+  __device__ __forceinline__ static int src(int j) {
+    constexpr unsigned ZS = (unsigned)(Z - G_::shift[e] % Z);  // (j - s) mod Z = (j + Z - s) mod Z
+    const unsigned a = (unsigned)j + ZS;
+    return e * Z + (int)min(a, a - (unsigned)Z);
+  }
+  template <int e>
+  __device__ __forceinline__ static int ez() { return e * Z; }
+};
+
+template <class G_, int RB_, int SPLIT_>
+struct SpGeoRT {
+  using G = G_;
+  static constexpr int SPLIT = SPLIT_, RB = RB_, NT_MAX = 768, MINB = 1;
+  static constexpr int NE_MAX = G_::row_start[RB_];
+  static constexpr int NCOL_MAX = G_::KB + (RB_ > 4 ? RB_ : 4);
+  int Z, NT1, NT, R, NE, NCOL;
+  unsigned Z2;
+  uint32_t s2[NE_MAX];  // 2 * (shift mod Z)
+  uint32_t cb[NE_MAX];  // 2 * Z * column
+  uint32_t zs[NE_MAX];  // Z - shift mod Z
+  __device__ __forceinline__ int z() const { return Z; }
+  __device__ __forceinline__ int nt1() const { return NT1; }
+  __device__ __forceinline__ int nt() const { return NT; }
+  __device__ __forceinline__ int ne() const { return NE; }
+  __device__ __forceinline__ int ncol() const { return NCOL; }
+  __device__ __forceinline__ static constexpr bool full_lanes() { return false; }
+  template <int r>
+  __device__ __forceinline__ bool live() const { return r < R; }
+  template <int e>
+  __device__ __forceinline__ unsigned off(unsigned i2) const {
+    const unsigned u = i2 + s2[e];
+    return cb[e] + min(u, u - Z2);
+  }
+  template <int e>
+  __device__ __forceinline__ int src(int j) const {
+    const unsigned a = (unsigned)j + zs[e];
+    return e * Z + (int)min(a, a - (unsigned)Z);
+  }
+  template <int e>
+  __device__ __forceinline__ int ez() const { return e * Z; }
+};
+
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
+    k_qc_sp(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int num_iter, int early_stop,
             uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
             const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts) {
-  using S = QcShapeSP<G, Z, R, SPLIT>;
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT;
+  const int Z = geo.z(), NT = geo.nt(), NCOLZ = geo.ncol() * Z;
   extern __shared__ __half smh[];
-  __half *c2v = smh;                        // [NE][Z]
-  __half *tot = smh + (size_t)S::NE * Z;    // [NCOL][Z]
+  __half *c2v = smh;                              // [NE][Z]
+  __half *tot = smh + (size_t)geo.ne() * Z;       // [NCOL][Z]
   char *const totb = reinterpret_cast<char *>(tot);
   const int t = threadIdx.x;
-  const int h = t / S::NT1;
-  const int i = t - h * S::NT1;
-  const bool lane = i < Z;
+  const int h = t / geo.nt1();
+  const int i = t - h * geo.nt1();
+  const bool lane = geo.full_lanes() || i < Z;
   const int64_t b = blockIdx.x;
   const float *row = llr + b * (int64_t)P.n;
 
-  for (int v = t; v < S::NCOL * Z; v += S::NT) tot[v] = __float2half_rn(chan_value(P, row, v));
-  for (int q = t; q < S::NE * Z; q += S::NT) c2v[q] = __float2half_rn(0.0f);
+  for (int v = t; v < NCOLZ; v += NT) tot[v] = __float2half_rn(chan_value(P, row, v));
+  for (int q = t; q < geo.ne() * Z; q += NT) c2v[q] = __float2half_rn(0.0f);
   __syncthreads();
 
   int used = num_iter;
@@ -82,11 +148,12 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
       sfor<0, SPLIT>([&](auto hc) {
         constexpr int H = decltype(hc)::value;
         if (h != H) return;
-        const unsigned i2 = 2u * (tid_volatile() - H * S::NT1);
+        const unsigned i2 = 2u * (tid_volatile() - H * geo.nt1());
         const int il = (int)(i2 >> 1);
-        sfor<0, (R + SPLIT - 1) / SPLIT>([&](auto jc) {
+        sfor<0, (Geo::RB + SPLIT - 1) / SPLIT>([&](auto jc) {
           constexpr int r = decltype(jc)::value * SPLIT + H;
-          if constexpr (r < R) {
+          if constexpr (r < Geo::RB) {
+            if (!geo.template live<r>()) return;
             constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
             float ph[d];
             uint32_t sg = 0, hs = 0;
@@ -94,9 +161,9 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
-              const __half th = *reinterpret_cast<const __half *>(totb + vn_off2<G, Z, e>(i2));
+              const __half th = *reinterpret_cast<const __half *>(totb + geo.template off<e>(i2));
               hs ^= (uint32_t)__half_as_ushort(th);
-              const float x = __half2float(th) - __half2float(c2v[e * Z + il]);
+              const float x = __half2float(th) - __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
               ph[p] = sp_phi(fabsf(x));
               ssum += ph[p];
@@ -107,7 +174,7 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
               constexpr int p = e - e0;
               const float m = fminf(sp_phi(fmaxf(ssum - ph[p], 1e-12f)), 30.0f);
               const bool neg = (par ^ (sg >> p)) & 1u;
-              c2v[e * Z + il] = __float2half_rn(neg ? -m : m);
+              c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
             synx |= hs;
           }
@@ -127,19 +194,17 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
       sfor<0, SPLIT>([&](auto hc) {
         constexpr int H = decltype(hc)::value;
         if (h != H) return;
-        const int j = (int)tid_volatile() - H * S::NT1;
-        sfor<0, (S::NCOL + SPLIT - 1) / SPLIT>([&](auto cc) {
+        const int j = (int)tid_volatile() - H * geo.nt1();
+        sfor<0, (Geo::NCOL_MAX + SPLIT - 1) / SPLIT>([&](auto cc) {
           constexpr int c = decltype(cc)::value * SPLIT + H;
-          if constexpr (c < S::NCOL) {
+          if constexpr (c < Geo::NCOL_MAX) {
+            if (c >= geo.ncol()) return;
             float sum = chan_value(P, row, c * Z + j);
             constexpr int q0 = G::col_start[c], q1 = G::col_start[c + 1];
             sfor<q0, q1>([&](auto qc) {
               constexpr int e = G::col_entry[decltype(qc)::value];
-              if constexpr (G::row[e] < R) {
-                constexpr unsigned ZS = (unsigned)(Z - G::shift[e] % Z);  // (j - s) mod Z = (j + Z - s) mod Z
-                const unsigned a = (unsigned)j + ZS;
-                const unsigned src = min(a, a - (unsigned)Z);
-                sum += __half2float(c2v[e * Z + src]);
+              if constexpr (G::row[e] < Geo::RB) {
+                if (geo.template live<G::row[e]>()) sum += __half2float(c2v[geo.template src<e>(j)]);
               }
             });
             tot[c * Z + j] = __float2half_rn(fminf(fmaxf(sum, -40.0f), 40.0f));
@@ -154,30 +219,48 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
   if (iters_used && t == 0) iters_used[b] = used;
   if (llr_out) {
     float *o = llr_out + b * (int64_t)P.n_full;
-    for (int v = t; v < P.n_full; v += S::NT)
-      o[v] = v < S::NCOL * Z ? -__half2float(tot[v]) : -chan_value(P, row, v);
+    for (int v = t; v < P.n_full; v += NT) o[v] = v < NCOLZ ? -__half2float(tot[v]) : -chan_value(P, row, v);
   }
   unsigned err = 0;
-  for (int v = t; v < P.k; v += S::NT) {
+  for (int v = t; v < P.k; v += NT) {
     const uint8_t hd = (-__half2float(tot[v])) > 0.0f;
     if (hard_k) hard_k[b * (int64_t)P.k + v] = hd;
     if (ref) err += (hd != ref[b * (int64_t)P.k + v]);
   }
   if (ref && counts) {
-    __shared__ unsigned red[S::NT / 32];
+    __shared__ unsigned red[Geo::NT_MAX / 32];
 #pragma unroll
     for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
     if ((t & 31) == 0) red[t >> 5] = err;
     __syncthreads();
     if (t == 0) {
       unsigned long long tt = 0;
-      for (int w = 0; w < S::NT / 32; ++w) tt += red[w];
+      for (int w = 0; w < NT / 32; ++w) tt += red[w];
       if (tt) {
         atomicAdd(&counts[0], tt);
         atomicAdd(&counts[1], 1ULL);
       }
     }
   }
+}
+
+template <class Geo>
+int launch_sp(const Geo &geo, int nt, size_t smem, const QcChanParams &P, const float *llr, int64_t B,
+              int num_iter, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,
+              const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
+  auto kern = k_qc_sp<Geo>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
+    const int64_t nb = B - b0 < 0x7fffffff ? B - b0 : 0x7fffffff;
+    kern<<<(unsigned)nb, nt, smem, s>>>(P, geo, llr + b0 * P.n, num_iter, early_stop,
+                                        hard_k ? hard_k + b0 * P.k : nullptr,
+                                        llr_out ? llr_out + b0 * P.n_full : nullptr,
+                                        iters_used ? iters_used + b0 : nullptr, ref ? ref + b0 * P.k : nullptr,
+                                        counts);
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
 }
 
 template <class G, int Z, int R, int SPLIT>
@@ -187,19 +270,41 @@ int launch_qc_sp(const QcChanParams &P, const float *llr, int64_t B, int num_ite
   (void)alpha;
   using S = QcShapeSP<G, Z, R, SPLIT>;
   static_assert(S::SMEM <= 227 * 1024, "sum-product messages do not fit in shared memory");
-  auto kern = k_qc_sp<G, Z, R, SPLIT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
-  for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
-    const int64_t nb = B - b0 < 0x7fffffff ? B - b0 : 0x7fffffff;
-    kern<<<(unsigned)nb, S::NT, S::SMEM, s>>>(P, llr + b0 * P.n, num_iter, early_stop,
-                                              hard_k ? hard_k + b0 * P.k : nullptr,
-                                              llr_out ? llr_out + b0 * P.n_full : nullptr,
-                                              iters_used ? iters_used + b0 : nullptr,
-                                              ref ? ref + b0 * P.k : nullptr, counts);
+  return launch_sp(SpGeoCT<G, Z, R, SPLIT>{}, S::NT, S::SMEM, P, llr, B, num_iter, early_stop, hard_k, llr_out,
+                   iters_used, ref, counts, s);
+}
+
+// runtime-geometry sum-product instance: any Z with NT1 * SPLIT <= 768 and any
+// R <= RB whose messages fit in shared memory
+template <class G, int RB, int SPLIT>
+int launch_qc_sprt(const QcChanParams &P, int R, const uint16_t *s_mod_z, const int32_t *col, const float *llr,
+                   int64_t B, int num_iter, float alpha, int early_stop, uint8_t *hard_k, float *llr_out,
+                   int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
+  (void)alpha;
+  using Geo = SpGeoRT<G, RB, SPLIT>;
+  static_assert(sizeof(Geo) + sizeof(QcChanParams) + 96 <= 32000, "kernel parameters too large");
+  const int Z = P.z;
+  if (R < 1 || R > RB) return fail(LS_EINVAL, "ls_qc_decode: row count outside the runtime-geometry instance");
+  Geo geo;
+  geo.Z = Z;
+  geo.NT1 = ((Z + 31) / 32) * 32;
+  geo.NT = geo.NT1 * SPLIT;
+  if (geo.NT > Geo::NT_MAX) return fail(LS_EINVAL, "ls_qc_decode: lifting size too large for this instance");
+  geo.R = R;
+  geo.NE = G::row_start[R];
+  geo.NCOL = G::KB + (R > 4 ? R : 4);
+  geo.Z2 = 2u * (unsigned)Z;
+  const size_t smem = 2ull * ((size_t)geo.NE * Z + (size_t)geo.NCOL * Z);
+  if (smem > 227 * 1024)
+    return fail(LS_EINVAL, "ls_qc_decode: sum-product messages of this code do not fit in shared memory; "
+                           "use the exact decoder");
+  for (int e = 0; e < Geo::NE_MAX; ++e) {
+    geo.s2[e] = 2u * s_mod_z[e];
+    geo.cb[e] = 2u * (unsigned)Z * (unsigned)col[e];
+    geo.zs[e] = (unsigned)(Z - s_mod_z[e]);
   }
-  e = cudaGetLastError();
-  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+  return launch_sp(geo, geo.NT, smem, P, llr, B, num_iter, early_stop, hard_k, llr_out, iters_used, ref, counts,
+                   s);
 }
 
 }  // namespace lsb

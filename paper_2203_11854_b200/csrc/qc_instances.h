@@ -2,7 +2,8 @@
 // rows, threads per lane, kind).  Each becomes build/gen/qc_<...>.cu.
 // fp16x2 min-sum codes matching none of them use a runtime-geometry instance
 // (LSB_QC_RT_INSTANCES below); fp32 ones the runtime-Z kernel in bp_fast.cu;
-// sum-product fast mode exists only for these instances.
+// sum-product fast mode uses these instances or a runtime-geometry one
+// (LSB_QC_SPRT_INSTANCES) when its messages fit in shared memory.
 //   1,384,24 / 1,384,46 : config 2 (k=8448 n=16896), dead rows pruned / all
 //   1,192,{24,45,46}    : configs 3 and 4 (k=4096, n=8192 / 12288)
 //   2,26,{12,42}        : config 1 (k=256 n=512)
@@ -55,3 +56,11 @@
   Y(2, 22, 2)                  \
   Y(2, 42, 2)                  \
   Y(2, 42, 4)
+
+// Runtime-geometry sum-product instances (base graph, row bound RB, threads
+// per lane); per-edge fp16 messages must fit in shared memory.
+#define LSB_QC_SPRT_INSTANCES(W) \
+  W(1, 24, 2)                    \
+  W(1, 46, 2)                    \
+  W(2, 22, 2)                    \
+  W(2, 42, 2)

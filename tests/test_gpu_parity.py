@@ -424,6 +424,42 @@ def test_fp16x2_runtime_geometry_equals_specialised_instance():
                 assert torch.equal(a[key], g[key]), (prune, es, key)
 
 
+@pytest.mark.parametrize("k,n,m,ebno", [(792, 1584, 2, 2.5), (200, 600, 2, 3.0), (3520, 5280, 4, 6.0),
+                                        (120, 240, 2, 3.5)])
+def test_sum_product_runtime_geometry_decoder(k, n, m, ebno):
+    """Sum-product fast mode on codes with no specialised instance (runtime
+    geometry): converged blocks identical to the reference's sum-product."""
+    code = lb.LdpcCode5G(k, n)
+    assert not lb.ldpc.qc_has_kernel(code, variant="sum-product")
+    B = 41 if k < 3000 else 13
+    bits, llr = _oracle_llrs(k, n, m, ebno, B, 23)
+    res = lb.qc_decode(llr, code, 20, "sum-product", early_stop=True, ref_bits=bits, want_iters=True)
+    hard = res["hard"].cpu().numpy()
+    ref_hard, _, it_o = O.decode(llr, O.code(k, n), 20, "sum-product", 0.75, True)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    ok_fast = (hard == bits).all(axis=1)
+    conv = (it_o <= 16) & ok_ref
+    assert conv.sum() >= B // 4
+    assert np.array_equal(hard[conv], ref_hard[conv])
+    assert (ok_ref != ok_fast).sum() <= max(1, B // 12)
+    it = res["iters"].cpu().numpy()
+    assert abs(it[conv].mean() - it_o[conv].mean()) <= 1.5
+    # same answer through the public API
+    assert np.array_equal(lb.ldpc5g_decode(llr, code, 20, "sum-product", mode="fast"), hard)
+
+
+def test_sum_product_runtime_geometry_equals_specialised_instance():
+    k, n = 8448, 16896
+    bits, llr = _oracle_llrs(k, n, 4, 4.6, 6, 4)
+    code = lb.LdpcCode5G(k, n)
+    for es in (True, False):
+        kw = dict(early_stop=es, want_llr=True, want_iters=True, prune=True)
+        a = lb.qc_decode(llr, code, 20, "sum-product", **kw)
+        g = lb.qc_decode(llr, code, 20, "sum-product", generic=True, **kw)
+        for key in ("hard", "llr", "iters"):
+            assert torch.equal(a[key], g[key]), (es, key)
+
+
 def test_fp16x2_noiseless_round_trip_any_lifting_size():
     # (rate-0.8 codes of the synthetic graph do not recover their punctured
     # columns even noiselessly, in the reference too, so none are listed)
