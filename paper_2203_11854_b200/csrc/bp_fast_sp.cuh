@@ -9,7 +9,7 @@
 // the variable update is a pure gather, total[c][j] = chan + sum over the
 // column's entries of c2v[e][(j - s_e) mod Z].
 //   CN phase (thread = lane i, row slot h): v2c = total - c2v_old,
-//            phi(x) = -log(tanh(x/2)) (ex2/rcp/lg2 MUFU, fp32), S = sum phi,
+//            phi(x) = -log(tanh(x/2)) (ex2/rcp/lg2 MUFU, fp32, base 2), S = sum phi,
 //            c2v_new = sign * clip(phi(max(S - phi_e, 1e-12)), 0, 30)
 //   VN phase (thread = lane j, column slot): gather + clip +-40
 // Shared memory: E_live*Z halves of messages + NCOL*Z halves of posteriors
@@ -33,16 +33,39 @@ struct QcShapeSP {
   static constexpr int MINB = NT >= 384 ? 1 : (384 / NT);
 };
 
-// phi(x) = -log(tanh(x / 2)) on the reference's clip range [1e-12, 40]
-// (3 MUFU: ex2, rcp, lg2; branch-free).  phi(x) = ln((1 + u) / (1 - u)) with
-// u = e^-x; for small x the denominator 1 - u comes from its Taylor series
-// (no cancellation).
-__device__ __forceinline__ float sp_phi(float x) {
-  x = fminf(fmaxf(x, 1e-12f), 40.0f);
-  const float u = __expf(-x);
-  const float series = x * fmaf(x, fmaf(x, fmaf(x, -1.0f / 24.0f, 1.0f / 6.0f), -0.5f), 1.0f);
-  const float om = x < 0.0625f ? series : 1.0f - u;
-  return __logf(__fdividef(1.0f + u, om));
+// phi(x) = -log(tanh(x/2)) on the reference's clip range [1e-12, 40], in
+// base-2 units: sp_phi2(y) = phi(y ln2) / ln2 for y = x log2(e), so that
+// 2^-y = e^-x.  The check-node sums run in these units (the second phi then
+// needs no rescaling of its argument), and only the outgoing message is
+// converted back to natural LLR units.  phi = log2((1 + u) / (1 - u)) with
+// u = 2^-y; 1 - u comes from its Taylor series for small y (no cancellation).
+// Flush-to-zero MUFU forms (ex2, rcp, lg2: 3 MUFU, no denormal fix-ups): every
+// operand here is a normal float.
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLn2 = 0.693147180559945309f, kLog2e = 1.442695040888963407f;
+constexpr float kPhiLo2 = 1e-12f * kLog2e, kPhiHi2 = 40.0f * kLog2e;
+
+__device__ __forceinline__ float sp_phi2(float y) {
+  y = fminf(fmaxf(y, kPhiLo2), kPhiHi2);
+  const float u = ex2_ftz(-y);
+  // 1 - 2^-y = y ln2 - (y ln2)^2 / 2 + (y ln2)^3 / 6 - ...
+  const float series = y * fmaf(y, fmaf(y, kLn2 * kLn2 * kLn2 / 6.0f, -kLn2 * kLn2 / 2.0f), kLn2);
+  const float om = y < 0.09f ? series : 1.0f - u;
+  return lg2_ftz((1.0f + u) * rcp_ftz(om));
 }
 
 template <class G, int Z, int E>
@@ -165,14 +188,14 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               hs ^= (uint32_t)__half_as_ushort(th);
               const float x = __half2float(th) - __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
-              ph[p] = sp_phi(fabsf(x));
+              ph[p] = sp_phi2(fabsf(x) * kLog2e);
               ssum += ph[p];
             });
             const uint32_t par = __popc(sg) & 1u;
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
-              const float m = fminf(sp_phi(fmaxf(ssum - ph[p], 1e-12f)), 30.0f);
+              const float m = fminf(sp_phi2(ssum - ph[p]) * kLn2, 30.0f);
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
