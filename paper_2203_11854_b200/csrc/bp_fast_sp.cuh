@@ -41,22 +41,6 @@ struct QcShapeSP {
 // u = 2^-y; 1 - u comes from its Taylor series for small y (no cancellation).
 // Flush-to-zero MUFU forms (ex2, rcp, lg2: 3 MUFU, no denormal fix-ups): every
 // operand here is a normal float.
-__device__ __forceinline__ float ex2_ftz(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float lg2_ftz(float x) {
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp_ftz(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-constexpr float kLn2 = 0.693147180559945309f, kLog2e = 1.442695040888963407f;
 constexpr float kPhiLo2 = 1e-12f * kLog2e, kPhiHi2 = 40.0f * kLog2e;
 
 __device__ __forceinline__ float sp_phi2(float y) {

@@ -90,15 +90,16 @@ __global__ void k_map_bits(const uint8_t *__restrict__ bits, int64_t nsym, int m
 __device__ __forceinline__ void normal_pair(int64_t q, uint64_t seed, uint64_t sid, float2 &n0, float2 &n1) {
   uint4 r = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)sid, (uint32_t)(sid >> 32)),
                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-  // uniforms in (0,1] and [0,1)
-  float u0 = ((r.x >> 8) + 1) * (1.0f / 16777216.0f), u1 = (r.y >> 8) * (1.0f / 16777216.0f);
-  float u2 = ((r.z >> 8) + 1) * (1.0f / 16777216.0f), u3 = (r.w >> 8) * (1.0f / 16777216.0f);
-  float rad0 = sqrtf(-2.0f * logf(u0)), rad1 = sqrtf(-2.0f * logf(u2));
-  float s0, c0, s1, c1;
-  sincospif(2.0f * u1, &s0, &c0);
-  sincospif(2.0f * u3, &s1, &c1);
-  n0 = make_float2(rad0 * c0, rad0 * s0);
-  n1 = make_float2(rad1 * c1, rad1 * s1);
+  // Box-Muller on uniforms u in (0,1] (radius) and angles in [-pi, pi):
+  // rad = sqrt(-2 ln u) = sqrt(-2 ln2 log2 u); one SFU op each for the log,
+  // the square root, the sine and the cosine
+  constexpr float k24 = 1.0f / 16777216.0f, kTwoPi24 = 6.283185307179586f / 16777216.0f;
+  const float u0 = (float)((r.x >> 8) + 1) * k24, u2 = (float)((r.z >> 8) + 1) * k24;
+  const float a1 = fmaf((float)(r.y >> 8), kTwoPi24, -3.14159265358979f);
+  const float a3 = fmaf((float)(r.w >> 8), kTwoPi24, -3.14159265358979f);
+  const float rad0 = sqrt_ftz(-2.0f * kLn2 * lg2_ftz(u0)), rad1 = sqrt_ftz(-2.0f * kLn2 * lg2_ftz(u2));
+  n0 = make_float2(rad0 * cos_ftz(a1), rad0 * sin_ftz(a1));
+  n1 = make_float2(rad1 * cos_ftz(a3), rad1 * sin_ftz(a3));
 }
 
 __global__ void k_awgn(const float2 *__restrict__ x, int64_t count, float sigma, uint64_t seed,
@@ -121,25 +122,23 @@ __global__ void k_awgn(const float2 *__restrict__ x, int64_t count, float sigma,
 // Fused map_bits -> awgn -> demap for Gray QAM (the Pipeline's fast chain):
 // coded bits [nsym*m] in, f32 LLRs [nsym*m] out, no symbol arrays in HBM.
 // Same points, noise stream and arithmetic order as k_map_bits + k_awgn
-// (y is bit-identical); the per-axis log-sum-exp runs in f32
-// (|dLLR| ~1e-6 relative to the f64 demapper, inside the 1e-4 tolerance).
+// (y is bit-identical); the per-axis log-sum-exp runs in f32, base 2, on the
+// SFU (ex2 / lg2; |dLLR| ~1e-6 against the f64 demapper, inside the 1e-4
+// tolerance).
 struct QamAxesF {
   float amp[16];
   int lab[16];
 };
 
-template <int HALF>
+template <int HALF, bool VEC>
 __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, const float2 *__restrict__ pts,
                             float sigma, float inv_no, uint64_t seed, uint64_t sid, int64_t q0, const QamAxesF A,
                             int maxlog, float *__restrict__ llr) {
   constexpr int L = 1 << HALF, M = 2 * HALF;
+  const float inv_no2 = inv_no * kLog2e;
   __shared__ float s_amp[L];
-  __shared__ int s_lab[L];
   __shared__ float2 s_pts[L * L];
-  if (threadIdx.x < L) {
-    s_amp[threadIdx.x] = A.amp[threadIdx.x];
-    s_lab[threadIdx.x] = A.lab[threadIdx.x];
-  }
+  if (threadIdx.x < L) s_amp[threadIdx.x] = A.amp[threadIdx.x];
   for (int p = threadIdx.x; p < L * L; p += blockDim.x) s_pts[p] = pts[p];
   __syncthreads();
   const int64_t npair = (nsym + 1) / 2;
@@ -147,23 +146,37 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
        q += (int64_t)gridDim.x * blockDim.x) {
     float2 nz[2];
     normal_pair(q0 + q, seed, sid, nz[0], nz[1]);
+    // VEC: the pair's 2M bit bytes in M/2 32-bit loads and its 2M LLRs in
+    // M/2 16-byte stores (full pairs only; needs 4-byte aligned bits and
+    // 16-byte aligned LLRs)
+    const bool full = VEC && 2 * q + 1 < nsym;
+    uint32_t w[VEC ? M / 2 : 1];
+    if (full) {
+      const uint32_t *b4 = reinterpret_cast<const uint32_t *>(bits + 2 * q * M);
+#pragma unroll
+      for (int k = 0; k < (VEC ? M / 2 : 1); ++k) w[k] = b4[k];
+    }
+    float out[2][M];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t s = 2 * q + u;
       if (s >= nsym) break;
       int label = 0;
 #pragma unroll
-      for (int t = 0; t < M; ++t) label = (label << 1) | (bits[s * M + t] & 1);
+      for (int t = 0; t < M; ++t) {
+        const int bi = u * M + t;
+        const uint32_t bt = full ? (w[bi >> 2] >> (8 * (bi & 3))) : bits[s * M + t];
+        label = (label << 1) | (bt & 1);
+      }
       const float2 x = s_pts[label];
       const float yv[2] = {x.x + sigma * nz[u].x, x.y + sigma * nz[u].y};
-      float out[M];
 #pragma unroll
       for (int ax = 0; ax < 2; ++ax) {
-        float lg[L];
+        float lg[L];  // logits in base-2 units
 #pragma unroll
         for (int l = 0; l < L; ++l) {
           const float d = yv[ax] - s_amp[l];
-          lg[l] = -(d * d) * inv_no;
+          lg[l] = -(d * d) * inv_no2;
         }
 #pragma unroll
         for (int t = 0; t < HALF; ++t) {
@@ -179,16 +192,27 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
             float s1 = 0.0f, s0 = 0.0f;
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-              if (((l ^ (l >> 1)) >> sh) & 1) s1 += __expf(lg[l] - mx1);
-              else s0 += __expf(lg[l] - mx0);
+              if (((l ^ (l >> 1)) >> sh) & 1) s1 += ex2_ftz(lg[l] - mx1);
+              else s0 += ex2_ftz(lg[l] - mx0);
             }
-            v += __logf(s1) - __logf(s0);  // the max terms contribute exactly 1 each
+            v += lg2_ftz(s1) - lg2_ftz(s0);  // the max terms contribute exactly 1 each
           }
-          out[2 * t + ax] = v;
+          out[u][2 * t + ax] = v * kLn2;
         }
       }
+      if (!full) {
 #pragma unroll
-      for (int j = 0; j < M; ++j) llr[s * M + j] = out[j];
+        for (int j = 0; j < M; ++j) llr[s * M + j] = out[u][j];
+      }
+    }
+    if (full) {
+      float4 *o4 = reinterpret_cast<float4 *>(llr + 2 * q * M);
+#pragma unroll
+      for (int k = 0; k < (VEC ? M / 2 : 1); ++k) {
+        const int j = 4 * k;
+        o4[k] = make_float4(out[j / M][j % M], out[(j + 1) / M][(j + 1) % M], out[(j + 2) / M][(j + 2) % M],
+                            out[(j + 3) / M][(j + 3) % M]);
+      }
     }
   }
 }
@@ -720,12 +744,17 @@ int ls_modem_qam_at(const uint8_t *bits, int64_t offset, int64_t nsym, int m, co
   cudaStream_t s = as_stream(stream);
   const unsigned g = grid_for((nsym + 1) / 2, 256);
   const int64_t q0 = offset / 2;
+  const bool vec = ((uintptr_t)bits % 4 == 0) && ((uintptr_t)llr % 16 == 0);
+#define LSB_MODEM(H)                                                                                           \
+  (vec ? k_modem_qam<H, true><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr) \
+       : k_modem_qam<H, false><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr))
   switch (m) {
-    case 2: k_modem_qam<1><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
-    case 4: k_modem_qam<2><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
-    case 6: k_modem_qam<3><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
-    default: k_modem_qam<4><<<g, 256, 0, s>>>(bits, nsym, pp, sigma, inv, seed, stream_id, q0, A, ml, llr); break;
+    case 2: LSB_MODEM(1); break;
+    case 4: LSB_MODEM(2); break;
+    case 6: LSB_MODEM(3); break;
+    default: LSB_MODEM(4); break;
   }
+#undef LSB_MODEM
   LS_CHECK_LAUNCH("ls_modem_qam");
   return LS_OK;
 }
