@@ -355,6 +355,30 @@ def test_fast_decoders_agree_on_a_large_batch():
         assert (b != ref).sum() <= 4, key
 
 
+def test_full_bench_size_properties():
+    """BASELINE.json config 2 at its full size (65,536 codewords, 4.4 GB of
+    LLRs): size-independent properties the oracle cannot check at this scale.
+    Noiseless channel LLRs must decode to the payload in every codeword for
+    the pair kernel (fixed 20 iterations) and the persistent early-stop
+    kernel (<= 2 iterations with the dead rows pruned), with fused error
+    counts of zero; the encoder's codewords satisfy H c = 0 on a sample."""
+    B = 65536
+    code = lb.LdpcCode5G(8448, 16896)
+    payload = lb.binary_source([B, 8448], lb.RngStream(77, 5), device=True)
+    tx = lb.ldpc5g_encode(payload, code, device=True)
+    full = code.encode_full(payload[:64].cpu().numpy())
+    assert not code.pcm.syndrome(full).any()
+    llr = (tx.to(torch.float32) * 16.0 - 8.0).contiguous()
+    for es in (False, True):
+        r = lb.qc_decode(llr, code, 20, "min-sum", early_stop=es, ref_bits=payload, want_iters=True,
+                         precision="fp16x2")
+        assert r["counts"].cpu().tolist() == [0, 0]
+        assert torch.equal(r["hard"], payload)
+        it = r["iters"]
+        assert bool((it == 20).all()) if not es else bool((it <= 2).all() and (it >= 1).all())
+    del llr, tx
+
+
 def test_fast_decoder_noiseless_round_trip_and_early_stop():
     for k, n in [(500, 1000), (100, 300), (8448, 16896), (4096, 12288), (256, 1536)]:
         code = lb.LdpcCode5G(k, n)
