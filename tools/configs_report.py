@@ -87,8 +87,9 @@ def config4(quick):
 def config5(quick):
     """Decoder-only table: every lifting size in [32, 384],
     BG1 rate 1/2 and BG2 rate 1/3, 5-50 fixed iterations, min-sum and scaled
-    min-sum on the fp16x2 decoder (specialised instance where compiled, else
-    the runtime-geometry kernel) and sum-product where an instance exists."""
+    min-sum on the fp16x2 decoder and sum-product (boxplus) on the fp16-message
+    decoder (specialised instance where compiled, else the runtime-geometry
+    kernel)."""
     iters = [5, 10, 20, 50]
     zs = [z for z in lb.ldpc.LIFTING_SIZES if 32 <= z <= 384] if not quick else [96, 384]
     rows = []
@@ -105,9 +106,6 @@ def config5(quick):
             edges = code.pcm.num_edges
             live = int(lb._lib.lib().ls_qc_live_rows(code.handle))
             for variant in ("min-sum", "scaled-min-sum", "sum-product"):
-                if variant == "sum-product" and not lb.ldpc.qc_has_kernel(code, variant=variant):
-                    rows.append({"bg": bg, "z": z, "variant": variant, "note": "no sum-product instance"})
-                    continue
                 prec = "fp32" if variant == "sum-product" else "fp16x2"
                 spec = lb.ldpc.qc_has_kernel(code, prec, variant=variant)
                 for it in iters:
