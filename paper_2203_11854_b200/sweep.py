@@ -246,7 +246,7 @@ class Pipeline:
                                 mode="exact", early_stop=self.bp_early_stop, device=True)
         return payload, dec
 
-    def run_batch(self, ebno_db: float, batch_size: int, rng: RngStream, chunk: int = 8192):
+    def run_batch(self, ebno_db: float, batch_size: int, rng: RngStream, chunk: int = 4096):
         """Simulate one batch; returns (payload, decoded) numpy bit arrays (sweep.py:347-364).
 
         The batch runs in row chunks; each chunk's results are copied to
