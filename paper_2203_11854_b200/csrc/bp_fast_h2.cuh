@@ -163,8 +163,9 @@ struct H2State {
 };
 
 // Check-node phase of one iteration for the calling thread's rows; returns
-// the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B).
-template <class Geo>
+// the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B), or 0
+// when SYN is off (fixed-iteration decoding needs no syndrome).
+template <class Geo, bool SYN = true>
 __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base, int h, bool lane, __half2 al2,
                                          bool scaled, const Geo &geo) {
   using G = typename Geo::G;
@@ -191,7 +192,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           constexpr int e = decltype(ec)::value;
           constexpr int p = e - e0;
           const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
-          hs ^= tw;
+          if constexpr (SYN) hs ^= tw;
           const __half2 pp = u2h(h2_int<p>());
           const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
           uint32_t sgn;
@@ -237,7 +238,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         st.M1[j] = n1;
         st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
         st.IX[j] = nix;
-        synx |= hs;
+        if constexpr (SYN) synx |= hs;
       }
     });
   });
@@ -335,7 +336,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
   __syncthreads();
 }
 
-template <class Geo>
+template <class Geo, bool ES>
 __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_fast_h2(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
                  float alpha, int early_stop, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
@@ -374,8 +375,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
 
   int doneA = 0, doneB = hasB ? 0 : 1;
   for (int it = 0; it < num_iter; ++it) {
-    const uint32_t synx = h2_cn(st, base, h, lane, al2, scaled, geo);
-    if (early_stop && it > 0) {
+    const uint32_t synx = h2_cn<Geo, ES>(st, base, h, lane, al2, scaled, geo);
+    if (ES && early_stop && it > 0) {
       // per-codeword syndrome of the posterior left by iteration `it`
       const int badA = __syncthreads_or(lane && ((synx >> 15) & 1u));
       const int badB = __syncthreads_or(lane && (synx >> 31));
@@ -557,7 +558,7 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
     cudaFreeAsync(next, s);
     return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
   }
-  auto kern = k_qc_fast_h2<Geo>;
+  auto kern = early_stop ? k_qc_fast_h2<Geo, true> : k_qc_fast_h2<Geo, false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   const int64_t chunk = 2LL * 0x3fffffff;
