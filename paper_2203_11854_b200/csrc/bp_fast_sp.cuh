@@ -124,7 +124,7 @@ struct SpGeoRT {
   __device__ __forceinline__ int ez() const { return e * Z; }
 };
 
-template <class Geo>
+template <class Geo, bool ES>
 __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_sp(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int num_iter, int early_stop,
             uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
               const __half th = *reinterpret_cast<const __half *>(totb + geo.template off<e>(i2));
-              hs ^= (uint32_t)__half_as_ushort(th);
+              if constexpr (ES) hs ^= (uint32_t)__half_as_ushort(th);
               const float x = __half2float(th) - __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
               ph[p] = sp_phi2(fabsf(x) * kLog2e);
@@ -183,12 +183,12 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
-            synx |= hs;
+            if constexpr (ES) synx |= hs;
           }
         });
       });
     }
-    if (early_stop && it > 0) {
+    if (ES && it > 0) {
       if (!__syncthreads_or(lane && ((synx >> 15) & 1u))) {  // fp16 sign bit
         used = it;
         break;
@@ -255,7 +255,7 @@ template <class Geo>
 int launch_sp(const Geo &geo, int nt, size_t smem, const QcChanParams &P, const float *llr, int64_t B,
               int num_iter, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,
               const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
-  auto kern = k_qc_sp<Geo>;
+  auto kern = early_stop ? k_qc_sp<Geo, true> : k_qc_sp<Geo, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
