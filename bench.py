@@ -377,7 +377,7 @@ def e2e_chain(a, pipe, rank, world, dist, steps=3):
             "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys"}
 
 
-def e2e_decode(a, pipe, rank, world, dist, steps=3):
+def e2e_decode(a, pipe, rank, world, dist, steps=5):
     """Drop-in decoder with HOST buffers: pinned f32 LLRs in, decoded bits out
     (ldpc5g_decode(llr, code, mode='fast'))."""
     import torch

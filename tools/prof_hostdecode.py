@@ -19,7 +19,7 @@ _, llr = pipe._llr(6.0, B, lb.RngStream(1, 2))
 host = torch.empty(llr.shape, dtype=torch.float32, pin_memory=True)
 host.copy_(llr)
 del llr
-for chunk in (16384, 8192, 4096, 2048, 8192):
+for chunk in (2048, 2048, 2048, 8192, 2048):
     for _ in range(2):
         ldpc._decode_host_pipelined(host, pipe.ldpc, 20, "min-sum", 0.75, False, "fp16x2", chunk=chunk)
     torch.cuda.synchronize()
