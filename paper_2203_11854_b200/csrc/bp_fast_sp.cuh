@@ -43,13 +43,28 @@ struct QcShapeSP {
 // operand here is a normal float.
 constexpr float kPhiLo2 = 1e-12f * kLog2e, kPhiHi2 = 40.0f * kLog2e;
 
-__device__ __forceinline__ float sp_phi2(float y) {
-  y = fminf(fmaxf(y, kPhiLo2), kPhiHi2);
-  const float u = ex2_ftz(-y);
+// 1 - 2^-y without cancellation: its Taylor series for small y
+__device__ __forceinline__ float sp_one_minus(float y, float u) {
   // 1 - 2^-y = y ln2 - (y ln2)^2 / 2 + (y ln2)^3 / 6 - ...
   const float series = y * fmaf(y, fmaf(y, kLn2 * kLn2 * kLn2 / 6.0f, -kLn2 * kLn2 / 2.0f), kLn2);
-  const float om = y < 0.09f ? series : 1.0f - u;
-  return lg2_ftz((1.0f + u) * rcp_ftz(om));
+  return y < 0.09f ? series : 1.0f - u;
+}
+
+// phi of the clipped argument y; also returns ratio = 2^phi = (1 + u) / (1 - u)
+__device__ __forceinline__ float sp_phi2(float y, float &ratio) {
+  y = fminf(fmaxf(y, kPhiLo2), kPhiHi2);
+  const float u = ex2_ftz(-y);
+  ratio = (1.0f + u) * rcp_ftz(sp_one_minus(y, u));
+  return lg2_ftz(ratio);
+}
+
+// phi(S - phi_e) for an edge of a check with S = sum of phi: the 2^-(S - phi_e)
+// it needs is 2^-S (once per check) times the edge's 2^phi_e, so the second
+// phi costs two SFU operations (rcp, lg2) instead of three
+__device__ __forceinline__ float sp_phi2_excl(float d, float e2s, float ratio) {
+  d = fmaxf(d, kPhiLo2);
+  const float u = e2s * ratio;  // = 2^-d; only used as 1 + u and, for d >= 0.09, 1 - u
+  return lg2_ftz((1.0f + u) * rcp_ftz(sp_one_minus(d, u)));
 }
 
 template <class G, int Z, int E>
@@ -162,7 +177,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
           if constexpr (r < Geo::RB) {
             if (!geo.template live<r>()) return;
             constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            float ph[d];
+            float ph[d], rt[d];
             uint32_t sg = 0, hs = 0;
             float ssum = 0.0f;
             sfor<e0, e1>([&](auto ec) {
@@ -172,14 +187,15 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               if constexpr (ES) hs ^= (uint32_t)__half_as_ushort(th);
               const float x = __half2float(th) - __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
-              ph[p] = sp_phi2(fabsf(x) * kLog2e);
+              ph[p] = sp_phi2(fabsf(x) * kLog2e, rt[p]);
               ssum += ph[p];
             });
             const uint32_t par = __popc(sg) & 1u;
+            const float e2s = ex2_ftz(-ssum);
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
-              const float m = fminf(sp_phi2(ssum - ph[p]) * kLn2, 30.0f);
+              const float m = fminf(sp_phi2_excl(ssum - ph[p], e2s, rt[p]) * kLn2, 30.0f);
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
