@@ -41,4 +41,4 @@ ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1])
 print(f"batch {a.batch} iters {a.iters}: {ms:.3f} ms/launch, "
-      f"{a.batch * a.k / ms / 1e6:.3f} Gbit/s, counts {counts.tolist()}")
+      f"{a.batch * a.k / ms / 1e6:.3f} Gbit/s, counts summed over {a.reps} launches {counts.tolist()}")
