@@ -276,6 +276,8 @@ def run_b200(a, rank, world, local_rank):
         line["e2e_decode_only"] = e2e_decode(a, pipe, rank, world, dist)
     if not a.early_stop:
         line["early_stop_variant"] = early_stop_rate(a, pipe, rank, world, dist)
+    if a.variant != "sum-product":
+        line["sum_product_variant"] = sum_product_rate(a, pipe, rank, world, dist)
     if not a.no_exact and rank == 0:
         line["exact_mode"] = exact_rate(a, pipe)
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -340,6 +342,50 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
             "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
             "note": "persistent fp16x2 kernel: each SM keeps two codeword slots busy and refills a slot "
                     "as soon as its codeword's syndrome is satisfied"}
+
+
+def sum_product_rate(a, pipe, rank, world, dist, steps=2):
+    """The reference's default BP variant (sum-product, ldpc.py:139-143) on the
+    same chain, fixed iterations: fp16 per-edge messages on chip, fp32 math."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+    from paper_2203_11854_b200 import _lib as L
+
+    B = a.batch
+    counts = L.zeros((2,), "int64")
+    dec = []
+
+    def one(i):
+        payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (700 + i)))
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        lb.qc_decode(llr, pipe.ldpc, a.iters, "sum-product", early_stop=False, ref_bits=payload, want_hard=False,
+                     counts=counts)
+        d1.record()
+        dec.append((d0, d1))
+
+    one(-1)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    dec.clear()
+    counts.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        one(i)
+    e1.record()
+    torch.cuda.synchronize()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm[0])
+    c = counts.cpu().tolist()
+    return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
+            "decoder_ms_per_launch": sum(d0.elapsed_time(d1) for d0, d1 in dec) / steps,
+            "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
+            "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi)"}
 
 
 def _wall_max(dist, secs):
