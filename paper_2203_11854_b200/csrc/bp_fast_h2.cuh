@@ -448,8 +448,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   uint32_t *tot = smw;
   uint32_t *chn = smw + SPLIT * NV;
   __shared__ unsigned red[Geo::NT_MAX / 32];
-  __shared__ long long slot_cw[2];
-  __shared__ int slot_it[2], slot_new[2];
+  __shared__ long long slot_cw[2], pend;
+  __shared__ int slot_it[2], slot_new[2], pend_new;
   const int t = threadIdx.x;
   const int h = t / geo.nt1();
   const int i = t - h * geo.nt1();
@@ -460,24 +460,32 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   H2State<Geo::NR> st;
 #pragma unroll
   for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+  // codewords are claimed one ahead of need: the pending codeword's channel
+  // LLRs are prefetched into L2 while the slots iterate, so a refill reads
+  // them from L2 instead of waiting on HBM
+  auto claim = [&]() -> long long {
+    const unsigned long long c = atomicAdd(next, 1ULL);
+    return (long long)c < batch ? (long long)c : -1;
+  };
   if (t == 0) {
     slot_cw[0] = slot_cw[1] = -1;
     slot_it[0] = slot_it[1] = 0;
+    pend = claim();
   }
   __syncthreads();
   auto chan_word = [&](int v) { return chn[v]; };  // channel words are always cached here
   for (;;) {
     // ---- refill empty slots
     if (t == 0) {
+      pend_new = 0;
       for (int q = 0; q < 2; ++q) {
         slot_new[q] = 0;
-        if (slot_cw[q] < 0) {
-          const unsigned long long c = atomicAdd(next, 1ULL);
-          if ((long long)c < batch) {
-            slot_cw[q] = (long long)c;
-            slot_it[q] = 0;
-            slot_new[q] = 1;
-          }
+        if (slot_cw[q] < 0 && pend >= 0) {
+          slot_cw[q] = pend;
+          slot_it[q] = 0;
+          slot_new[q] = 1;
+          pend = claim();
+          pend_new = 1;
         }
       }
     }
@@ -485,6 +493,11 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     const long long cw0 = slot_cw[0], cw1 = slot_cw[1];
     if (cw0 < 0 && cw1 < 0) return;
     const int new0 = slot_new[0], new1 = slot_new[1];
+    if (pend_new && pend >= 0) {
+      const char *row = reinterpret_cast<const char *>(llr + pend * (int64_t)P.n);
+      for (int64_t off = 128 * (int64_t)t; off < 4 * (int64_t)P.n; off += 128 * (int64_t)NT)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+    }
     if (new0 | new1) {
       unsigned short *c16 = reinterpret_cast<unsigned short *>(chn);
       unsigned short *t16 = reinterpret_cast<unsigned short *>(tot);
