@@ -152,6 +152,24 @@ def to_device(x, dtype=None):
     return t.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
+_side_streams: dict = {}
+
+
+def side_stream(name: str):
+    """A long-lived side stream per (device, name).  Reusing it across calls
+    keeps the caching allocator's per-stream blocks reusable (a fresh stream
+    per call would strand them and force new device allocations)."""
+    t = torch()
+    key = (t.cuda.current_device(), name)
+    st = _side_streams.get(key)
+    if st is None:
+        with _lock:
+            st = _side_streams.get(key)
+            if st is None:
+                st = _side_streams[key] = t.cuda.Stream()
+    return st
+
+
 def to_host(t):
     """CUDA tensor -> numpy (synchronising on the current stream)."""
     return t.cpu().numpy()

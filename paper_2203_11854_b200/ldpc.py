@@ -235,7 +235,7 @@ def _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, prec
     B = src.shape[0]
     out = torch.empty((B, code.k), dtype=torch.uint8, pin_memory=True)
     main = torch.cuda.current_stream()
-    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    h2d, d2h = L.side_stream("h2d"), L.side_stream("d2h")
     dev = L.device()
     for lo in range(0, B, chunk):
         hi = min(B, lo + chunk)

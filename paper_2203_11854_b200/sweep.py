@@ -261,7 +261,7 @@ class Pipeline:
         ph = torch.empty((batch_size, k), dtype=torch.uint8, pin_memory=True)
         dh = torch.empty((batch_size, k), dtype=torch.uint8, pin_memory=True)
         main = torch.cuda.current_stream()
-        copy = torch.cuda.Stream()
+        copy = L.side_stream("run_batch_d2h")
         for lo in range(0, batch_size, chunk):
             hi = min(batch_size, lo + chunk)
             p, d = self.run_batch_device(ebno_db, hi - lo, rng, lo)
