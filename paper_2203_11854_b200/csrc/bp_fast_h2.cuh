@@ -157,6 +157,13 @@ __device__ __forceinline__ void h2_emit(const QcChanParams &P, const uint32_t *t
 
 // per-thread compressed check state of the thread's NR rows (registers once
 // the phase functions are inlined with compile-time row indices)
+// base entry e sits in a degree-1 column (an extension parity bit): its
+// variable hears from no other check, so posterior - own message = channel
+template <class G, int E>
+__host__ __device__ constexpr bool col_deg1() {
+  return G::col_start[G::col[E] + 1] - G::col_start[G::col[E]] == 1;
+}
+
 template <int NR>
 struct H2State {
   uint32_t M1[NR], M2[NR], IX[NR], SG[NR], SG2[NR];
@@ -165,9 +172,15 @@ struct H2State {
 // Check-node phase of one iteration for the calling thread's rows; returns
 // the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B), or 0
 // when SYN is off (fixed-iteration decoding needs no syndrome).
-template <class Geo, bool SYN = true>
+// D1 (fixed iterations, no posterior output): an edge into a degree-1
+// extension-parity variable takes its variable-to-check message straight
+// from the cached channel word -- the min-sum value posterior - own message
+// without the fp16 round trip -- and those variables' posteriors are never
+// formed (h2_vn skips them).
+template <class Geo, bool SYN = true, bool D1 = false>
 __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base, int h, bool lane, __half2 al2,
-                                         bool scaled, const Geo &geo) {
+                                         bool scaled, const Geo &geo, const char *cbase = nullptr) {
+  static_assert(!(SYN && D1), "the degree-1 shortcut leaves those posteriors unformed");
   using G = typename Geo::G;
   constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
   uint32_t synx = 0;
@@ -191,18 +204,23 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         sfor<e0, e1>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int p = e - e0;
-          const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
-          if constexpr (SYN) hs ^= tw;
-          const __half2 pp = u2h(h2_int<p>());
-          const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
-          uint32_t sgn;
-          if constexpr (packed) {
-            sgn = (osg << (15 - p)) & 0x80008000u;
+          __half2 x;
+          if constexpr (D1 && col_deg1<G, e>()) {
+            x = u2h(*reinterpret_cast<const uint32_t *>(cbase + geo.template off<e>(i4)));
           } else {
-            const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-            sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+            const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
+            if constexpr (SYN) hs ^= tw;
+            const __half2 pp = u2h(h2_int<p>());
+            const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
+            uint32_t sgn;
+            if constexpr (packed) {
+              sgn = (osg << (15 - p)) & 0x80008000u;
+            } else {
+              const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+              sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+            }
+            x = __hsub2(u2h(tw), u2h(mag | sgn));
           }
-          const __half2 x = __hsub2(u2h(tw), u2h(mag | sgn));
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
           // argmin: per-half mask select (HSET2 + LOP3); first minimum wins
@@ -247,26 +265,29 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
 
 // Variable-node phase: posteriors = clip(chan + sum of the new messages).
 // `chan_word(v)` supplies the channel half2 of VN v when it is not cached.
-template <class Geo, class ChanFn>
+template <class Geo, bool D1 = false, class ChanFn>
 __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot, const uint32_t *chn, char *base,
                                       int h, bool lane, int t, ChanFn chan_word, const Geo &geo) {
   using G = typename Geo::G;
   constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
-  const int NV = geo.nv(), NT = geo.nt();
-  if (geo.chn_smem() && NV % 4 == 0) {
+  const int NVA = geo.nv(), NT = geo.nt();
+  // with D1 only the columns left of the degree-1 extension parities are
+  // reset / accumulated / combined (array strides stay NVA)
+  const int NV = D1 ? (G::KB + 4) * geo.z() : NVA;
+  if (geo.chn_smem() && NV % 4 == 0 && NVA % 4 == 0) {
     // 128-bit shared accesses: 4 posteriors (8 messages) per instruction
     uint4 *t4 = reinterpret_cast<uint4 *>(tot);
     const uint4 *c4 = reinterpret_cast<const uint4 *>(chn);
     for (int v = t; v < NV / 4; v += NT) {
       t4[v] = c4[v];
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) t4[q * (NV / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
+      for (int q = 1; q < SPLIT; ++q) t4[q * (NVA / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
     }
   } else {
     for (int v = t; v < NV; v += NT) {
       tot[v] = geo.chn_smem() ? chn[v] : chan_word(v);
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) tot[q * NV + v] = 0u;
+      for (int q = 1; q < SPLIT; ++q) tot[q * NVA + v] = 0u;
     }
   }
   __syncthreads();
@@ -277,7 +298,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
     constexpr int H = decltype(hc)::value;
     if (h != H) return;
     const unsigned i4 = 4u * tid_volatile() - 4u * H * geo.nt1();
-    char *const arr = base + 4u * H * NV;
+    char *const arr = base + 4u * H * NVA;
     sfor<0, NR>([&](auto jc) {
       constexpr int j = decltype(jc)::value;
       constexpr int r = j * SPLIT + H;
@@ -290,6 +311,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
           sfor<e0, e1>([&](auto ec) {
             constexpr int e = decltype(ec)::value;
             constexpr int p = e - e0;
+            if constexpr (D1 && col_deg1<G, e>()) return;
             uint32_t *tp = reinterpret_cast<uint32_t *>(arr + geo.template off<e>(i4));
             const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
             uint32_t sgn;
@@ -307,13 +329,13 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
     });
   });
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
-  if (NV % 4 == 0) {
+  if (NV % 4 == 0 && NVA % 4 == 0) {
     uint4 *t4 = reinterpret_cast<uint4 *>(tot);
     for (int v = t; v < NV / 4; v += NT) {
       uint4 a = t4[v];
 #pragma unroll
       for (int q = 1; q < SPLIT; ++q) {
-        const uint4 o = t4[q * (NV / 4) + v];
+        const uint4 o = t4[q * (NVA / 4) + v];
         a.x = h2u(__hadd2(u2h(a.x), u2h(o.x)));
         a.y = h2u(__hadd2(u2h(a.y), u2h(o.y)));
         a.z = h2u(__hadd2(u2h(a.z), u2h(o.z)));
@@ -329,14 +351,14 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
     for (int v = t; v < NV; v += NT) {
       __half2 acc = u2h(tot[v]);
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * NV + v]));
+      for (int q = 1; q < SPLIT; ++q) acc = __hadd2(acc, u2h(tot[q * NVA + v]));
       tot[v] = h2u(__hmin2(__hmax2(acc, lo), hi));
     }
   }
   __syncthreads();
 }
 
-template <class Geo, bool ES>
+template <class Geo, bool ES, bool D1>
 __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_fast_h2(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
                  float alpha, int early_stop, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
@@ -375,7 +397,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
 
   int doneA = 0, doneB = hasB ? 0 : 1;
   for (int it = 0; it < num_iter; ++it) {
-    const uint32_t synx = h2_cn<Geo, ES>(st, base, h, lane, al2, scaled, geo);
+    const uint32_t synx = h2_cn<Geo, ES, D1>(st, base, h, lane, al2, scaled, geo,
+                                             reinterpret_cast<const char *>(chn));
     if (ES && early_stop && it > 0) {
       // per-codeword syndrome of the posterior left by iteration `it`
       const int badA = __syncthreads_or(lane && ((synx >> 15) & 1u));
@@ -392,7 +415,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     } else {
       __syncthreads();
     }
-    h2_vn(st, tot, chn, base, h, lane, t, chan_word, geo);
+    h2_vn<Geo, D1>(st, tot, chn, base, h, lane, t, chan_word, geo);
   }
   if (!doneA)
     h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwA, rowA, 0, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
@@ -571,7 +594,10 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
     cudaFreeAsync(next, s);
     return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
   }
-  auto kern = early_stop ? k_qc_fast_h2<Geo, true> : k_qc_fast_h2<Geo, false>;
+  // D1 needs the cached channel words and gives up the extension-parity
+  // posteriors, so it serves fixed-iteration calls without an LLR output
+  auto kern = early_stop ? k_qc_fast_h2<Geo, true, false>
+                         : ((llr_out || !chn_smem) ? k_qc_fast_h2<Geo, false, false> : k_qc_fast_h2<Geo, false, true>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   const int64_t chunk = 2LL * 0x3fffffff;
