@@ -172,15 +172,15 @@ struct H2State {
 // Check-node phase of one iteration for the calling thread's rows; returns
 // the OR of the row syndromes (bit 15: codeword A, bit 31: codeword B), or 0
 // when SYN is off (fixed-iteration decoding needs no syndrome).
-// D1 (fixed iterations, no posterior output): an edge into a degree-1
+// D1 (no posterior output requested): an edge into a degree-1
 // extension-parity variable takes its variable-to-check message straight
 // from the cached channel word -- the min-sum value posterior - own message
 // without the fp16 round trip -- and those variables' posteriors are never
-// formed (h2_vn skips them).
+// formed (h2_vn skips them); with SYN their syndrome sign is channel + own
+// message, the same fp16 sum the variable update would have stored.
 template <class Geo, bool SYN = true, bool D1 = false>
 __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base, int h, bool lane, __half2 al2,
                                          bool scaled, const Geo &geo, const char *cbase = nullptr) {
-  static_assert(!(SYN && D1), "the degree-1 shortcut leaves those posteriors unformed");
   using G = typename Geo::G;
   constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR;
   uint32_t synx = 0;
@@ -206,7 +206,19 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           constexpr int p = e - e0;
           __half2 x;
           if constexpr (D1 && col_deg1<G, e>()) {
-            x = u2h(*reinterpret_cast<const uint32_t *>(cbase + geo.template off<e>(i4)));
+            const uint32_t cw = *reinterpret_cast<const uint32_t *>(cbase + geo.template off<e>(i4));
+            x = u2h(cw);
+            if constexpr (SYN) {  // the unformed posterior's sign: channel + own message
+              const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
+              uint32_t sgn;
+              if constexpr (packed) {
+                sgn = (osg << (15 - p)) & 0x80008000u;
+              } else {
+                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
+                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
+              }
+              hs ^= h2u(__hadd2(u2h(cw), u2h(mag | sgn)));
+            }
           } else {
             const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
             if constexpr (SYN) hs ^= tw;
@@ -459,7 +471,7 @@ __device__ __forceinline__ void h2_reset_half(H2State<Geo::NR> &st, int h, int n
 // while its partner keeps iterating.  Same per-codeword arithmetic and
 // iteration semantics as k_qc_fast_h2 (the halves never interact).  Needs the
 // channel LLRs cached in shared memory (the launcher checks).
-template <class Geo>
+template <class Geo, bool D1>
 __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     k_qc_fast_h2p(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
                   float alpha, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
@@ -538,7 +550,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
       __syncthreads();
     }
     // ---- one iteration for both slots
-    const uint32_t synx = h2_cn(st, base, h, lane, al2, scaled, geo);
+    const uint32_t synx = h2_cn<Geo, true, D1>(st, base, h, lane, al2, scaled, geo,
+                                               reinterpret_cast<const char *>(chn));
     const int bad0 = __syncthreads_or(lane && ((synx >> 15) & 1u));
     const int bad1 = __syncthreads_or(lane && (synx >> 31));
     bool freed = false;
@@ -559,7 +572,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
       __syncthreads();
       if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
     }
-    h2_vn(st, tot, chn, base, h, lane, t, chan_word, geo);
+    h2_vn<Geo, D1>(st, tot, chn, base, h, lane, t, chan_word, geo);
     if (t == 0) {
       slot_it[0] += 1;
       slot_it[1] += 1;
@@ -576,7 +589,7 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
               const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
   cudaError_t e;
   if (chn_smem && early_stop && B >= 4) {  // persistent slot-refilling decoder
-    auto kp = k_qc_fast_h2p<Geo>;
+    auto kp = llr_out ? k_qc_fast_h2p<Geo, false> : k_qc_fast_h2p<Geo, true>;
     e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
     int dev = 0, sms = 148, per_sm = 1;
