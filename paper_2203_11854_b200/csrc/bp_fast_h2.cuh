@@ -235,11 +235,22 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           }
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
-          // argmin: per-half mask select (HSET2 + LOP3); first minimum wins
-          const uint32_t lt = __hlt2_mask(a, u2h(n1));
-          nix = (lt & h2_int<p>()) | (~lt & nix);
-          n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
-          n1 = h2u(__hmin2(u2h(n1), a));
+          // argmin: per-half mask select (HSET2 + LOP3); first minimum wins.
+          // The first two edges start from min1 = min2 = +inf, which the
+          // compiler cannot fold through HMNMX2, so they are written out.
+          if constexpr (p == 0) {
+            n1 = h2u(a);  // n2 stays +inf, argmin 0
+          } else if constexpr (p == 1) {
+            const uint32_t lt = __hlt2_mask(a, u2h(n1));
+            nix = lt & h2_int<1>();
+            n2 = h2u(__hmax2(u2h(n1), a));
+            n1 = h2u(__hmin2(u2h(n1), a));
+          } else {
+            const uint32_t lt = __hlt2_mask(a, u2h(n1));
+            nix = (lt & h2_int<p>()) | (~lt & nix);
+            n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
+            n1 = h2u(__hmin2(u2h(n1), a));
+          }
           if constexpr (packed) {
             if constexpr (p == 15)
               sg |= xw & 0x80008000u;
