@@ -6,7 +6,8 @@
 //   posterior   half2 {A, B} per VN in shared memory
 //   CN state    M1, M2 = half2 {min_A, min_B} (alpha-scaled), IX = half2
 //               {argmin_A, argmin_B} (small integers are exact in fp16), sign
-//               bits in one word for d <= 16 (A: bits 0..15, B: 16..31) or two
+//               bits A: bits 0..15, B: 16..31 of one word (edges 0..15) and of
+//               a second word (edges 16..31) for rows of degree above 16
 //   per edge    mag   = select(M1, M2, IX == {p,p})        (HSET2 + LOP3)
 //               cold  = mag | signs moved to bits 15/31     (SHF + LOP3)
 //               x     = t - cold                            (HADD2)
@@ -164,6 +165,25 @@ __host__ __device__ constexpr bool col_deg1() {
   return G::col_start[G::col[E] + 1] - G::col_start[G::col[E]] == 1;
 }
 
+// Sign bits of a row's edges: edge p < 16 in SG (codeword A at bit p, B at
+// bit 16 + p), edges 16..31 the same way in SG2, so every edge's sign moves
+// to the fp16 sign positions with one shift and a mask.
+template <int P>
+__device__ __forceinline__ uint32_t old_sign(uint32_t osg, uint32_t osg2) {
+  static_assert(P < 32, "row degree above 32");
+  constexpr int Q = P & 15;
+  return ((P < 16 ? osg : osg2) << (15 - Q)) & 0x80008000u;
+}
+template <int P>
+__device__ __forceinline__ void acc_sign(uint32_t &sg, uint32_t &sg2, uint32_t xw) {
+  constexpr int Q = P & 15;
+  uint32_t &t = P < 16 ? sg : sg2;
+  if constexpr (Q == 15)
+    t |= xw & 0x80008000u;
+  else
+    t |= __umulhi(xw, 1u << (17 + Q)) & (0x10001u << Q);  // xw >> (15 - Q)
+}
+
 template <int NR>
 struct H2State {
   uint32_t M1[NR], M2[NR], IX[NR], SG[NR], SG2[NR];
@@ -200,7 +220,8 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         // compare result (FMA pipe)
         const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
         const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
-        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, hs = 0u, nix = 0u;
+        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, nix = 0u;
+        [[maybe_unused]] uint32_t hs = 0u;
         sfor<e0, e1>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int p = e - e0;
@@ -210,28 +231,14 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
             x = u2h(cw);
             if constexpr (SYN) {  // the unformed posterior's sign: channel + own message
               const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-              uint32_t sgn;
-              if constexpr (packed) {
-                sgn = (osg << (15 - p)) & 0x80008000u;
-              } else {
-                const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-                sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
-              }
-              hs ^= h2u(__hadd2(u2h(cw), u2h(mag | sgn)));
+              hs ^= h2u(__hadd2(u2h(cw), u2h(mag | old_sign<p>(osg, osg2))));
             }
           } else {
             const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
             if constexpr (SYN) hs ^= tw;
             const __half2 pp = u2h(h2_int<p>());
             const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
-            uint32_t sgn;
-            if constexpr (packed) {
-              sgn = (osg << (15 - p)) & 0x80008000u;
-            } else {
-              const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-              sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
-            }
-            x = __hsub2(u2h(tw), u2h(mag | sgn));
+            x = __hsub2(u2h(tw), u2h(mag | old_sign<p>(osg, osg2)));
           }
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
@@ -251,24 +258,18 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
             n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
             n1 = h2u(__hmin2(u2h(n1), a));
           }
-          if constexpr (packed) {
-            if constexpr (p == 15)
-              sg |= xw & 0x80008000u;
-            else
-              sg |= __umulhi(xw, 1u << (17 + p)) & (0x10001u << p);  // xw >> (15 - p)
-          } else {
-            sg |= ((xw >> 15) & 1u) << p;
-            sg2 |= (xw >> 31) << p;
-          }
+          acc_sign<p>(sg, sg2, xw);
         });
-        constexpr uint32_t dm = (1u << d) - 1u;
+        constexpr uint32_t dm = (1u << (d < 16 ? d : 16)) - 1u;
         if constexpr (packed) {
           const uint32_t pa = __popc(sg & 0xFFFFu) & 1u, pb = __popc(sg >> 16) & 1u;
           st.SG[j] = sg ^ (((0u - pa) & dm) | ((0u - pb) & (dm << 16)));
         } else {
-          const uint32_t pa = __popc(sg) & 1u, pb = __popc(sg2) & 1u;
-          st.SG[j] = sg ^ ((0u - pa) & dm);
-          st.SG2[j] = sg2 ^ ((0u - pb) & dm);
+          constexpr uint32_t dm2 = (1u << (d - 16)) - 1u;
+          const uint32_t pa = (__popc(sg & 0xFFFFu) + __popc(sg2 & 0xFFFFu)) & 1u;
+          const uint32_t pb = (__popc(sg >> 16) + __popc(sg2 >> 16)) & 1u;
+          st.SG[j] = sg ^ (((0u - pa) & dm) | ((0u - pb) & (dm << 16)));
+          st.SG2[j] = sg2 ^ (((0u - pa) & dm2) | ((0u - pb) & (dm2 << 16)));
         }
         if (scaled) {
           n1 = h2u(__hmul2(u2h(n1), al2));
@@ -327,8 +328,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
       constexpr int r = j * SPLIT + H;
       if constexpr (r < Geo::RB) {
         if (lane && geo.template live<r>()) {
-          constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-          constexpr bool packed = d <= 16;
+          constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1];
           const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
           const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
           sfor<e0, e1>([&](auto ec) {
@@ -337,14 +337,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
             if constexpr (D1 && col_deg1<G, e>()) return;
             uint32_t *tp = reinterpret_cast<uint32_t *>(arr + geo.template off<e>(i4));
             const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-            uint32_t sgn;
-            if constexpr (packed) {
-              sgn = (osg << (15 - p)) & 0x80008000u;
-            } else {
-              const uint32_t a15 = p <= 15 ? (osg << (15 - p)) : (osg >> (p - 15));
-              sgn = (a15 & 0x8000u) | ((osg2 << (31 - p)) & 0x80000000u);
-            }
-            *tp = h2u(__hadd2(u2h(*tp), u2h(mag | sgn)));
+            *tp = h2u(__hadd2(u2h(*tp), u2h(mag | old_sign<p>(osg, osg2))));
           });
         }
       }
@@ -446,8 +439,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
 }
 
-// zero the check state of the refilled half(s): packed rows keep A in the low
-// and B in the high halves of every word; unpacked rows keep B's signs in SG2
+// zero the check state of the refilled half(s): every state word keeps
+// codeword A in its low and B in its high half
 template <class Geo>
 __device__ __forceinline__ void h2_reset_half(H2State<Geo::NR> &st, int h, int new0, int new1) {
   using G = typename Geo::G;
@@ -464,12 +457,8 @@ __device__ __forceinline__ void h2_reset_half(H2State<Geo::NR> &st, int h, int n
         st.M1[j] &= keep;
         st.M2[j] &= keep;
         st.IX[j] &= keep;
-        if constexpr (d <= 16) {
-          st.SG[j] &= keep;
-        } else {
-          if (new0) st.SG[j] = 0u;
-          if (new1) st.SG2[j] = 0u;
-        }
+        st.SG[j] &= keep;
+        if constexpr (d > 16) st.SG2[j] &= keep;
       }
     });
   });
