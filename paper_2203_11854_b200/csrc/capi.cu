@@ -173,30 +173,38 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
 #pragma unroll
       for (int ax = 0; ax < 2; ++ax) {
         float lg[L];  // logits in base-2 units
+        float top = -INFINITY;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
           const float d = yv[ax] - s_amp[l];
           lg[l] = -(d * d) * inv_no2;
+          top = fmaxf(top, lg[l]);
+        }
+        // APP: one exponential per level against the axis maximum, shared by
+        // the axis's bits (L instead of L * HALF SFU exponentials); the subset
+        // holding the maximum sums to >= 1, the other can only underflow when
+        // its log-sum is more than 126 below, where max-log is exact
+        float ex[L];
+        if (!maxlog) {
+#pragma unroll
+          for (int l = 0; l < L; ++l) ex[l] = ex2_ftz(lg[l] - top);
         }
 #pragma unroll
         for (int t = 0; t < HALF; ++t) {
           const int sh = HALF - 1 - t;
-          float mx1 = -INFINITY, mx0 = -INFINITY;
+          float mx1 = -INFINITY, mx0 = -INFINITY, s1 = 0.0f, s0 = 0.0f;
 #pragma unroll
           for (int l = 0; l < L; ++l) {  // level l carries Gray label l ^ (l >> 1)
-            if (((l ^ (l >> 1)) >> sh) & 1) mx1 = fmaxf(mx1, lg[l]);
-            else mx0 = fmaxf(mx0, lg[l]);
+            if (((l ^ (l >> 1)) >> sh) & 1) {
+              mx1 = fmaxf(mx1, lg[l]);
+              if (!maxlog) s1 += ex[l];
+            } else {
+              mx0 = fmaxf(mx0, lg[l]);
+              if (!maxlog) s0 += ex[l];
+            }
           }
           float v = mx1 - mx0;
-          if (!maxlog) {
-            float s1 = 0.0f, s0 = 0.0f;
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-              if (((l ^ (l >> 1)) >> sh) & 1) s1 += ex2_ftz(lg[l] - mx1);
-              else s0 += ex2_ftz(lg[l] - mx0);
-            }
-            v += lg2_ftz(s1) - lg2_ftz(s0);  // the max terms contribute exactly 1 each
-          }
+          if (!maxlog && s1 > 0.0f && s0 > 0.0f) v = lg2_ftz(s1) - lg2_ftz(s0);
           out[u][2 * t + ax] = v * kLn2;
         }
       }
