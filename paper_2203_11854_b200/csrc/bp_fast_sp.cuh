@@ -139,7 +139,21 @@ struct SpGeoRT {
   __device__ __forceinline__ int ez() const { return e * Z; }
 };
 
-template <class Geo, bool ES>
+// Degree-1 shortcut (D1, fixed iterations without a posterior output): an
+// extension-parity variable hears from one check only, so its message into
+// that check is the channel LLR (posterior minus own message); its posterior
+// stays the channel value in `tot`, its check-to-variable message is never
+// formed and its column is left out of the variable update.
+template <class G, int E>
+__host__ __device__ constexpr bool sp_col_deg1() {
+  return G::col_start[G::col[E] + 1] - G::col_start[G::col[E]] == 1;
+}
+template <class G, int C>
+__host__ __device__ constexpr bool sp_col_is_deg1() {
+  return G::col_start[C + 1] - G::col_start[C] == 1;
+}
+
+template <class Geo, bool ES, bool D1>
 __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_sp(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int num_iter, int early_stop,
             uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
@@ -185,7 +199,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               constexpr int p = e - e0;
               const __half th = *reinterpret_cast<const __half *>(totb + geo.template off<e>(i2));
               if constexpr (ES) hs ^= (uint32_t)__half_as_ushort(th);
-              const float x = __half2float(th) - __half2float(c2v[geo.template ez<e>() + il]);
+              float x = __half2float(th);
+              if constexpr (!(D1 && sp_col_deg1<G, e>())) x -= __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
               ph[p] = sp_phi2(fabsf(x) * kLog2e, rt[p]);
               ssum += ph[p];
@@ -195,6 +210,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
+              if constexpr (D1 && sp_col_deg1<G, e>()) return;
               const float m = fminf(sp_phi2_excl(ssum - ph[p], e2s, rt[p]) * kLn2, 30.0f);
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
@@ -221,6 +237,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
         sfor<0, (Geo::NCOL_MAX + SPLIT - 1) / SPLIT>([&](auto cc) {
           constexpr int c = decltype(cc)::value * SPLIT + H;
           if constexpr (c < Geo::NCOL_MAX) {
+            if constexpr (D1 && sp_col_is_deg1<G, c>()) return;
             if (c >= geo.ncol()) return;
             float sum = chan_value(P, row, c * Z + j);
             constexpr int q0 = G::col_start[c], q1 = G::col_start[c + 1];
@@ -271,7 +288,7 @@ template <class Geo>
 int launch_sp(const Geo &geo, int nt, size_t smem, const QcChanParams &P, const float *llr, int64_t B,
               int num_iter, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,
               const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
-  auto kern = early_stop ? k_qc_sp<Geo, true> : k_qc_sp<Geo, false>;
+  auto kern = early_stop ? k_qc_sp<Geo, true, false> : (llr_out ? k_qc_sp<Geo, false, false> : k_qc_sp<Geo, false, true>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
