@@ -83,6 +83,39 @@ struct H2GeoCT {
   __device__ __forceinline__ static constexpr bool live() { return true; }
   template <int e>
   __device__ __forceinline__ static unsigned off(unsigned i4) { return vn_off<G_, Z, e>(i4); }
+  template <int e>
+  __device__ __forceinline__ static unsigned coff(unsigned i4) { return vn_off<G_, Z, e>(i4); }
+};
+
+// Wrap-free layout of the fixed-iteration D1 kernel (k_qc_fast_h2w): the
+// posteriors of the NCA = k_b + 4 accumulated columns are stored twice per
+// column (2Z words, word Z + j = word j), and so are the channel words of the
+// degree-1 extension columns, so the check-node read of VN (c, (i + s) mod Z)
+// is the word c*2Z + i + s: the lane offset plus an immediate, no wrap.
+//   T   [NCA][2Z]             posteriors; slot 0's accumulator (first copy)
+//   A   [SPLIT-1][NCA][Z]     accumulators of slots 1..SPLIT-1
+//   C   [NCA][Z] ++ [NCD][2Z] channel words (extension columns doubled)
+template <class G_, int Z, int R, int SPLIT_>
+struct H2GeoCTW : H2GeoCT<G_, Z, R, SPLIT_> {
+  using G = G_;
+  static constexpr int NCA = G_::KB + 4, NCD = R > 4 ? R - 4 : 0;
+  static constexpr int T_W = NCA * 2 * Z, A_W = NCA * Z;
+  static constexpr int C_OFF = T_W + (SPLIT_ - 1) * A_W;  // channel region, in words
+  static constexpr int C_W = NCA * Z + NCD * 2 * Z;
+  static constexpr size_t SMEM = 4 * (size_t)(C_OFF + C_W);
+  static constexpr bool FITS = SMEM <= 225 * 1024;
+  template <int e>
+  __device__ __forceinline__ static unsigned off(unsigned i4) {
+    constexpr unsigned c = (unsigned)G_::col[e], s = (unsigned)(G_::shift[e] % Z);
+    static_assert(G_::col[e] < NCA, "wrap-free read of an extension column");
+    return 4u * (c * 2u * Z + s) + i4;
+  }
+  template <int e>
+  __device__ __forceinline__ static unsigned coff(unsigned i4) {
+    constexpr unsigned c = (unsigned)G_::col[e], s = (unsigned)(G_::shift[e] % Z);
+    static_assert(G_::col[e] >= NCA, "doubled channel words exist for extension columns only");
+    return 4u * ((unsigned)NCA * Z + (c - NCA) * 2u * Z + s) + i4;
+  }
 };
 
 template <class G_, int RB_, int SPLIT_>
@@ -107,6 +140,10 @@ struct H2GeoRT {
   __device__ __forceinline__ unsigned off(unsigned i4) const {
     const unsigned u = i4 + s4[e];
     return cb[e] + min(u, u - Z4);
+  }
+  template <int e>
+  __device__ __forceinline__ unsigned coff(unsigned i4) const {
+    return off<e>(i4);
   }
 };
 
@@ -227,7 +264,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           constexpr int p = e - e0;
           __half2 x;
           if constexpr (D1 && col_deg1<G, e>()) {
-            const uint32_t cw = *reinterpret_cast<const uint32_t *>(cbase + geo.template off<e>(i4));
+            const uint32_t cw = *reinterpret_cast<const uint32_t *>(cbase + geo.template coff<e>(i4));
             x = u2h(cw);
             if constexpr (SYN) {  // the unformed posterior's sign: channel + own message
               const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
@@ -439,6 +476,212 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
 }
 
+// Variable-node phase of the wrap-free layout (H2GeoCTW): posteriors =
+// clip(chan + sum of the new messages) over the NCA accumulated columns,
+// written to both copies of each column.  Slot 0 accumulates into T's first
+// copy, slot q > 0 into A[q-1]; these writes wrap (i + s) mod Z as usual.
+template <class Geo>
+__device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw, int h, int t) {
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR, Z = Geo::z(), NCA = Geo::NCA, NT = Geo::nt();
+  constexpr int Z4 = Z / 4;
+  static_assert(Z % 4 == 0, "wrap-free layout needs Z % 4 == 0");
+  uint4 *T4 = reinterpret_cast<uint4 *>(smw);
+  uint4 *A4 = reinterpret_cast<uint4 *>(smw + Geo::T_W);
+  const uint4 *C4 = reinterpret_cast<const uint4 *>(smw + Geo::C_OFF);
+  constexpr int NQ = NCA * Z4;  // uint4 words per accumulator
+  for (int v = t; v < NQ; v += NT) {
+    const int c = v / Z4, j = v - c * Z4;
+    T4[c * 2 * Z4 + j] = C4[v];
+#pragma unroll
+    for (int q = 1; q < SPLIT; ++q) A4[(q - 1) * NQ + v] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncthreads();
+  sfor<0, SPLIT>([&](auto hc) {
+    constexpr int H = decltype(hc)::value;
+    if (h != H) return;
+    const unsigned i4 = 4u * tid_volatile() - 4u * H * Geo::nt1();
+    constexpr unsigned STRIDE = H == 0 ? 2u * Z : (unsigned)Z;  // words per column
+    char *const arr = reinterpret_cast<char *>(H == 0 ? smw : smw + Geo::T_W + (H - 1) * Geo::A_W);
+    sfor<0, NR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      constexpr int r = j * SPLIT + H;
+      if constexpr (r < Geo::RB) {
+        constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1];
+        const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
+        const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
+        sfor<e0, e1>([&](auto ec) {
+          constexpr int e = decltype(ec)::value;
+          constexpr int p = e - e0;
+          if constexpr (col_deg1<G, e>()) return;
+          constexpr unsigned S4 = 4u * (unsigned)(G::shift[e] % Z);
+          constexpr unsigned CB = 4u * STRIDE * (unsigned)G::col[e];
+          const unsigned o = S4 == 0 ? CB + i4 : CB + min(i4 + S4, i4 + (S4 - 4u * Z));
+          uint32_t *tp = reinterpret_cast<uint32_t *>(arr + o);
+          const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
+          *tp = h2u(__hadd2(u2h(*tp), u2h(mag | old_sign<p>(osg, osg2))));
+        });
+      }
+      __syncthreads();
+    });
+  });
+  const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
+  for (int v = t; v < NQ; v += NT) {
+    const int c = v / Z4, j = v - c * Z4;
+    uint4 x = T4[c * 2 * Z4 + j];
+#pragma unroll
+    for (int q = 1; q < SPLIT; ++q) {
+      const uint4 o = A4[(q - 1) * NQ + v];
+      x.x = h2u(__hadd2(u2h(x.x), u2h(o.x)));
+      x.y = h2u(__hadd2(u2h(x.y), u2h(o.y)));
+      x.z = h2u(__hadd2(u2h(x.z), u2h(o.z)));
+      x.w = h2u(__hadd2(u2h(x.w), u2h(o.w)));
+    }
+    x.x = h2u(__hmin2(__hmax2(u2h(x.x), lo), hi));
+    x.y = h2u(__hmin2(__hmax2(u2h(x.y), lo), hi));
+    x.z = h2u(__hmin2(__hmax2(u2h(x.z), lo), hi));
+    x.w = h2u(__hmin2(__hmax2(u2h(x.w), lo), hi));
+    T4[c * 2 * Z4 + j] = x;
+    T4[c * 2 * Z4 + Z4 + j] = x;
+  }
+  __syncthreads();
+}
+
+// channel words of VN v for codewords A / B, no repetition (n <= buffer):
+// one load each, the same value as chan_value
+__device__ __forceinline__ uint32_t chan_word_norep(const QcChanParams &P, const float *rowA, const float *rowB,
+                                                    bool hasB, int v) {
+  float a, b;
+  if (v >= P.k && v < P.k_full) {
+    a = b = 40.0f;
+  } else if (v < 2 * P.z) {
+    a = b = -0.0f;
+  } else {
+    const int pos = v < P.k ? v - 2 * P.z : P.l1 + (v - P.k_full);
+    if (pos < P.n) {
+      a = -(0.0f + __ldg(rowA + pos));
+      b = hasB ? -(0.0f + __ldg(rowB + pos)) : 40.0f;
+    } else {  // never transmitted
+      a = -0.0f;
+      b = hasB ? -0.0f : 40.0f;
+    }
+  }
+  return h2u(__floats2half2_rn(a, b));
+}
+
+// Fixed-iteration fp16x2 min-sum decoder on the wrap-free layout: the
+// schedule and arithmetic of k_qc_fast_h2<Geo, false, true> (bit-identical
+// outputs), without the wrap arithmetic in the check-node reads.  Persistent:
+// each CTA walks codeword pairs blockIdx.x, +gridDim.x, ... and prefetches
+// the next pair's channel LLRs into L2 while it iterates on the current one,
+// so the load at the start of a pair hits L2.  Hard decisions and counts
+// only (no posterior output).
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT_MAX, 1)
+    k_qc_fast_h2w(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
+                  uint8_t *__restrict__ hard_k, int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
+                  unsigned long long *__restrict__ counts, int dbg) {
+  constexpr int Z = Geo::z(), NCA = Geo::NCA, NCD = Geo::NCD, NT = Geo::nt(), NVT = (NCA + NCD) * Z;
+  extern __shared__ uint32_t smw[];
+  uint32_t *C = smw + Geo::C_OFF;
+  __shared__ unsigned red[Geo::NT_MAX / 32];
+  const int t = threadIdx.x;
+  const int h = t / Geo::nt1();
+  const __half2 al2 = __float2half2_rn(alpha);
+  const bool scaled = alpha != 1.0f;
+  const bool norep = P.n <= P.buflen && !(dbg & 1);
+  const int64_t npairs = (batch + 1) / 2;
+  const char *base = reinterpret_cast<const char *>(smw);
+  // channel word w of VN v into the layout: C (extension columns twice) and
+  // both copies of T
+  auto put = [&](int v, uint32_t w) {
+    const int c = v / Z, j = v - c * Z;
+    if (c < NCA) {
+      C[v] = w;
+      smw[c * 2 * Z + j] = w;
+      smw[c * 2 * Z + Z + j] = w;
+    } else {
+      const int o = NCA * Z + (c - NCA) * 2 * Z + j;
+      C[o] = w;
+      C[o + Z] = w;
+    }
+  };
+  auto prefetch_pair = [&](int64_t pr) {
+    if (pr >= npairs || (dbg & 2)) return;
+    const int64_t cw0 = 2 * pr;
+    const int64_t bytes = 4 * (int64_t)P.n * (cw0 + 1 < batch ? 2 : 1);
+    const char *row = reinterpret_cast<const char *>(llr + cw0 * (int64_t)P.n);
+    for (int64_t off = 128 * (int64_t)t; off < bytes; off += 128 * (int64_t)NT)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+  };
+  prefetch_pair(blockIdx.x);
+  for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    const int64_t cwA = 2 * pr, cwB = cwA + 1;
+    const bool hasB = cwB < batch;
+    const float *rowA = llr + cwA * (int64_t)P.n;
+    const float *rowB = hasB ? rowA + P.n : rowA;
+    if (norep) {
+      // four independent loads in flight per thread
+      constexpr int U = 4;
+      for (int v0 = t; v0 < NVT; v0 += U * NT) {
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int v = v0 + u * NT;
+          w[u] = v < NVT ? chan_word_norep(P, rowA, rowB, hasB, v) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (v0 + u * NT < NVT) put(v0 + u * NT, w[u]);
+      }
+    } else {
+      for (int v = t; v < NVT; v += NT)
+        put(v, h2u(__floats2half2_rn(chan_value(P, rowA, v), hasB ? chan_value(P, rowB, v) : 40.0f)));
+    }
+    prefetch_pair(pr + gridDim.x);
+    H2State<Geo::NR> st;
+#pragma unroll
+    for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+    __syncthreads();
+    for (int it = 0; it < num_iter; ++it) {
+      h2_cn<Geo, false, true>(st, base, h, true, al2, scaled, Geo{}, reinterpret_cast<const char *>(C));
+      __syncthreads();
+      h2w_vn<Geo>(st, smw, h, t);
+    }
+    // hard decisions of the systematic columns (k <= KB * Z < NCA * Z)
+    auto emit = [&](int64_t cw, int hb) {
+      if (iters_used && t == 0) iters_used[cw] = num_iter;
+      unsigned err = 0;
+      for (int v = t; v < P.k; v += NT) {
+        const int c = v / Z, j = v - c * Z;
+        const uint32_t w = smw[c * 2 * Z + j];
+        const unsigned short hv = (unsigned short)(hb ? (w >> 16) : (w & 0xFFFFu));
+        const uint8_t hd = (-__half2float(__ushort_as_half(hv))) > 0.0f;
+        if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
+        if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
+      }
+      if (ref && counts) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+        if ((t & 31) == 0) red[t >> 5] = err;
+        __syncthreads();
+        if (t == 0) {
+          unsigned long long tt = 0;
+          for (int w = 0; w < NT / 32; ++w) tt += red[w];
+          if (tt) {
+            atomicAdd(&counts[0], tt);
+            atomicAdd(&counts[1], 1ULL);
+          }
+        }
+        __syncthreads();  // red[] is reused by the next emit
+      }
+    };
+    emit(cwA, 0);
+    if (hasB) emit(cwB, 1);
+    __syncthreads();  // the next pair's channel words overwrite T
+  }
+}
+
 // zero the check state of the refilled half(s): every state word keeps
 // codeword A in its low and B in its high half
 template <class Geo>
@@ -631,6 +874,27 @@ int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int nu
                       uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
                       unsigned long long *counts, cudaStream_t s) {
   using S = QcShapeH2<G, Z, R, SPLIT>;
+  using W = H2GeoCTW<G, Z, R, SPLIT>;
+  // fixed iterations, hard decisions only: the wrap-free layout when it fits
+  // (LSB_H2_WRAPFREE=0 forces the wrapped kernel, for the bit-identity test)
+  if constexpr (W::FITS && Z % 32 == 0 && R > 4) {
+    const char *env = getenv("LSB_H2_WRAPFREE");
+    if (!early_stop && !llr_out && S::CHN_SMEM && !(env && env[0] == '0')) {
+      auto kern = k_qc_fast_h2w<W>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::NT, W::SMEM);
+      const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
+      if (grid > 0)
+        kern<<<(unsigned)grid, S::NT, W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts,
+                                                    env ? atoi(env) >> 1 : 0);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+    }
+  }
   return launch_h2(H2GeoCT<G, Z, R, SPLIT>{}, S::NT, S::SMEM, S::CHN_SMEM, P, llr, B, num_iter, alpha, early_stop,
                    hard_k, llr_out, iters_used, ref, counts, s);
 }
