@@ -92,15 +92,19 @@ struct H2GeoCT {
 // column (2Z words, word Z + j = word j), and so are the channel words of the
 // degree-1 extension columns, so the check-node read of VN (c, (i + s) mod Z)
 // is the word c*2Z + i + s: the lane offset plus an immediate, no wrap.
-//   T   [NCA][2Z]             posteriors; slot 0's accumulator (first copy)
-//   A   [SPLIT-1][NCA][Z]     accumulators of slots 1..SPLIT-1
+//   T   [NCA][2Z]             posteriors; the accumulators of slots 0 and 1
+//   A   [SPLIT-2][NCA][Z]     accumulators of slots 2..SPLIT-1
 //   C   [NCA][Z] ++ [NCD][2Z] channel words (extension columns doubled)
 template <class G_, int Z, int R, int SPLIT_>
 struct H2GeoCTW : H2GeoCT<G_, Z, R, SPLIT_> {
   using G = G_;
   static constexpr int NCA = G_::KB + 4, NCD = R > 4 ? R - 4 : 0;
   static constexpr int T_W = NCA * 2 * Z, A_W = NCA * Z;
-  static constexpr int C_OFF = T_W + (SPLIT_ - 1) * A_W;  // channel region, in words
+  static constexpr int C_OFF = T_W + (SPLIT_ > 2 ? SPLIT_ - 2 : 0) * A_W;  // channel region, in words
+  // first word of slot q's accumulator for column c (see h2w_vn)
+  __host__ __device__ static constexpr int acc_word(int q, int c) {
+    return q == 0 ? c * 2 * Z : (q == 1 ? c * 2 * Z + Z : T_W + (q - 2) * A_W + c * Z);
+  }
   static constexpr int C_W = NCA * Z + NCD * 2 * Z;
   static constexpr size_t SMEM = 4 * (size_t)(C_OFF + C_W);
   static constexpr bool FITS = SMEM <= 225 * 1024;
@@ -257,7 +261,8 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         // compare result (FMA pipe)
         const __half2 o1 = u2h(st.M1[j]), od = u2h(st.M2[j]), oix = u2h(st.IX[j]);
         const uint32_t osg = st.SG[j], osg2 = st.SG2[j];
-        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u, nix = 0u;
+        uint32_t n1 = 0x7C007C00u, n2 = 0x7C007C00u, sg = 0u, sg2 = 0u;
+        __half2 wv = u2h(0u);
         [[maybe_unused]] uint32_t hs = 0u;
         sfor<e0, e1>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
@@ -279,19 +284,21 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           }
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
-          // argmin: per-half mask select (HSET2 + LOP3); first minimum wins.
-          // The first two edges start from min1 = min2 = +inf, which the
-          // compiler cannot fold through HMNMX2, so they are written out.
+          // argmin on the FMA pipe: w = argmin - p, kept as w' = u (w - 1)
+          // with u = (a >= min1) in {0, 1} (HSET2.BF + HFMA2), so a new
+          // minimum (u = 0) resets it to 0; first minimum wins.  The first
+          // two edges start from min1 = min2 = +inf, which the compiler
+          // cannot fold through HMNMX2, so they are written out.
           if constexpr (p == 0) {
             n1 = h2u(a);  // n2 stays +inf, argmin 0
           } else if constexpr (p == 1) {
-            const uint32_t lt = __hlt2_mask(a, u2h(n1));
-            nix = lt & h2_int<1>();
+            const __half2 u = __hge2(a, u2h(n1));
+            wv = __hneg2(u);
             n2 = h2u(__hmax2(u2h(n1), a));
             n1 = h2u(__hmin2(u2h(n1), a));
           } else {
-            const uint32_t lt = __hlt2_mask(a, u2h(n1));
-            nix = (lt & h2_int<p>()) | (~lt & nix);
+            const __half2 u = __hge2(a, u2h(n1));
+            wv = __hfma2(u, wv, __hneg2(u));
             n2 = h2u(__hmin2(u2h(n2), __hmax2(u2h(n1), a)));
             n1 = h2u(__hmin2(u2h(n1), a));
           }
@@ -316,7 +323,7 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
         // edge is reconstructed as min1 + diff (within 1 ulp of min2)
         st.M1[j] = n1;
         st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
-        st.IX[j] = nix;
+        st.IX[j] = d > 1 ? h2u(__hadd2(wv, u2h(h2_int<d - 1>()))) : 0u;
         if constexpr (SYN) synx |= hs;
       }
     });
@@ -476,33 +483,63 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cwB, rowB, 1, num_iter, hard_k, llr_out, iters_used, ref, counts, red);
 }
 
+// first barrier step j at which slot q (rows j * SPLIT + q < RB) touches
+// base column c, or -1
+template <class G, int SPLIT, int RB>
+__host__ __device__ constexpr int h2w_first_step(int q, int c) {
+  for (int j = 0; j * SPLIT + q < RB; ++j) {
+    const int r = j * SPLIT + q;
+    for (int e = G::row_start[r]; e < G::row_start[r + 1]; ++e)
+      if (G::col[e] == c) return j;
+  }
+  return -1;
+}
+
 // Variable-node phase of the wrap-free layout (H2GeoCTW): posteriors =
 // clip(chan + sum of the new messages) over the NCA accumulated columns,
-// written to both copies of each column.  Slot 0 accumulates into T's first
-// copy, slot q > 0 into A[q-1]; these writes wrap (i + s) mod Z as usual.
+// written to both copies of each column.  Both copies of T are dead once the
+// check-node phase is done, so slot 0 accumulates into T's first copy, slot 1
+// into its second copy and slot q >= 2 into A[q-2] (Geo::acc_word); these
+// writes wrap (i + s) mod Z as usual.
 template <class Geo>
-__device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw, int h, int t) {
+__device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw, int h, int t, int dbg = 0) {
   using G = typename Geo::G;
   constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR, Z = Geo::z(), NCA = Geo::NCA, NT = Geo::nt();
   constexpr int Z4 = Z / 4;
   static_assert(Z % 4 == 0, "wrap-free layout needs Z % 4 == 0");
-  uint4 *T4 = reinterpret_cast<uint4 *>(smw);
-  uint4 *A4 = reinterpret_cast<uint4 *>(smw + Geo::T_W);
+  uint4 *S4w = reinterpret_cast<uint4 *>(smw);
   const uint4 *C4 = reinterpret_cast<const uint4 *>(smw + Geo::C_OFF);
+  const char *Cb = reinterpret_cast<const char *>(smw + Geo::C_OFF);
   constexpr int NQ = NCA * Z4;  // uint4 words per accumulator
-  for (int v = t; v < NQ; v += NT) {
-    const int c = v / Z4, j = v - c * Z4;
-    T4[c * 2 * Z4 + j] = C4[v];
-#pragma unroll
-    for (int q = 1; q < SPLIT; ++q) A4[(q - 1) * NQ + v] = make_uint4(0u, 0u, 0u, 0u);
+  // No reset pass: the first row of slot q to touch column c (in barrier-step
+  // order) initialises the accumulator -- slot 0 as chan + message, slot q > 0
+  // as +0 + message -- so only columns a slot never touches are reset here
+  // (none for BG1 with two slots).
+  constexpr bool any_untouched = [] {
+    for (int q = 0; q < SPLIT; ++q)
+      for (int c = 0; c < NCA; ++c)
+        if (h2w_first_step<G, SPLIT, Geo::RB>(q, c) < 0) return true;
+    return false;
+  }();
+  if constexpr (any_untouched) {
+    sfor<0, NCA>([&](auto cc) {
+      constexpr int c = decltype(cc)::value;
+      for (int j = t; j < Z4; j += NT) {
+        if constexpr (h2w_first_step<G, SPLIT, Geo::RB>(0, c) < 0) S4w[Geo::acc_word(0, c) / 4 + j] = C4[c * Z4 + j];
+        sfor<1, SPLIT>([&](auto qc) {
+          constexpr int q = decltype(qc)::value;
+          if constexpr (h2w_first_step<G, SPLIT, Geo::RB>(q, c) < 0)
+            S4w[Geo::acc_word(q, c) / 4 + j] = make_uint4(0u, 0u, 0u, 0u);
+        });
+      }
+    });
+    __syncthreads();
   }
-  __syncthreads();
-  sfor<0, SPLIT>([&](auto hc) {
+  if (!(dbg & 8)) sfor<0, SPLIT>([&](auto hc) {
     constexpr int H = decltype(hc)::value;
     if (h != H) return;
     const unsigned i4 = 4u * tid_volatile() - 4u * H * Geo::nt1();
-    constexpr unsigned STRIDE = H == 0 ? 2u * Z : (unsigned)Z;  // words per column
-    char *const arr = reinterpret_cast<char *>(H == 0 ? smw : smw + Geo::T_W + (H - 1) * Geo::A_W);
+    char *const arr = reinterpret_cast<char *>(smw);
     sfor<0, NR>([&](auto jc) {
       constexpr int j = decltype(jc)::value;
       constexpr int r = j * SPLIT + H;
@@ -515,23 +552,32 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
           constexpr int p = e - e0;
           if constexpr (col_deg1<G, e>()) return;
           constexpr unsigned S4 = 4u * (unsigned)(G::shift[e] % Z);
-          constexpr unsigned CB = 4u * STRIDE * (unsigned)G::col[e];
-          const unsigned o = S4 == 0 ? CB + i4 : CB + min(i4 + S4, i4 + (S4 - 4u * Z));
-          uint32_t *tp = reinterpret_cast<uint32_t *>(arr + o);
+          constexpr unsigned c = (unsigned)G::col[e];
+          const unsigned lo4 = S4 == 0 ? i4 : min(i4 + S4, i4 + (S4 - 4u * Z));  // 4 * ((i + s) mod Z)
+          uint32_t *tp = reinterpret_cast<uint32_t *>(arr + 4u * Geo::acc_word(H, (int)c) + lo4);
           const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-          *tp = h2u(__hadd2(u2h(*tp), u2h(mag | old_sign<p>(osg, osg2))));
+          const __half2 msg = u2h(mag | old_sign<p>(osg, osg2));
+          constexpr bool first = h2w_first_step<G, SPLIT, Geo::RB>(H, (int)c) == j;
+          if constexpr (!first) {
+            *tp = h2u(__hadd2(u2h(*tp), msg));
+          } else if constexpr (H == 0) {
+            const uint32_t cw = *reinterpret_cast<const uint32_t *>(Cb + 4u * Z * c + lo4);
+            *tp = h2u(__hadd2(u2h(cw), msg));
+          } else {
+            *tp = h2u(__hadd2(u2h(0u), msg));  // +0 + m: the sum the zeroed accumulator gave
+          }
         });
       }
       __syncthreads();
     });
   });
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
-  for (int v = t; v < NQ; v += NT) {
+  if (!(dbg & 16)) for (int v = t; v < NQ; v += NT) {
     const int c = v / Z4, j = v - c * Z4;
-    uint4 x = T4[c * 2 * Z4 + j];
+    uint4 x = S4w[c * 2 * Z4 + j];
 #pragma unroll
     for (int q = 1; q < SPLIT; ++q) {
-      const uint4 o = A4[(q - 1) * NQ + v];
+      const uint4 o = S4w[(q == 1 ? c * 2 * Z4 + Z4 : Geo::T_W / 4 + (q - 2) * NQ + c * Z4) + j];
       x.x = h2u(__hadd2(u2h(x.x), u2h(o.x)));
       x.y = h2u(__hadd2(u2h(x.y), u2h(o.y)));
       x.z = h2u(__hadd2(u2h(x.z), u2h(o.z)));
@@ -541,10 +587,72 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
     x.y = h2u(__hmin2(__hmax2(u2h(x.y), lo), hi));
     x.z = h2u(__hmin2(__hmax2(u2h(x.z), lo), hi));
     x.w = h2u(__hmin2(__hmax2(u2h(x.w), lo), hi));
-    T4[c * 2 * Z4 + j] = x;
-    T4[c * 2 * Z4 + Z4 + j] = x;
+    S4w[c * 2 * Z4 + j] = x;
+    S4w[c * 2 * Z4 + Z4 + j] = x;
   }
   __syncthreads();
+}
+
+// block-wide sum of the per-thread error counts of one codeword; one bit /
+// block error update (every thread calls it)
+__device__ __forceinline__ void h2w_count(unsigned err, unsigned long long *counts, unsigned *red, int t, int NT) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+  if ((t & 31) == 0) red[t >> 5] = err;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tt = 0;
+    for (int w = 0; w < NT / 32; ++w) tt += red[w];
+    if (tt) {
+      atomicAdd(&counts[0], tt);
+      atomicAdd(&counts[1], 1ULL);
+    }
+  }
+  __syncthreads();  // red[] is reused by the next count
+}
+
+// hard decisions of both codewords of a pair from T's first copy, 16 bits
+// per thread: four 128-bit shared loads, one 128-bit store per codeword and
+// the reference bits compared with one 128-bit load (k % 16 == 0, Z % 16 == 0)
+template <class Geo>
+__device__ __forceinline__ void h2w_emit_vec(const QcChanParams &P, const uint32_t *smw, int64_t cwA, bool hasB,
+                                             int num_iter, uint8_t *hard_k, int32_t *iters_used, const uint8_t *ref,
+                                             unsigned long long *counts, unsigned *red, int t) {
+  constexpr int Z = Geo::z(), NT = Geo::nt();
+  if (iters_used && t == 0) {
+    iters_used[cwA] = num_iter;
+    if (hasB) iters_used[cwA + 1] = num_iter;
+  }
+  unsigned errA = 0, errB = 0;
+  for (int g = t; g < P.k / 16; g += NT) {
+    const int v0 = 16 * g, c = v0 / Z, j = v0 - c * Z;
+    uint4 rA = make_uint4(0u, 0u, 0u, 0u), rB = rA;
+    if (ref) {
+      rA = __ldg(reinterpret_cast<const uint4 *>(ref + cwA * (int64_t)P.k) + g);
+      if (hasB) rB = __ldg(reinterpret_cast<const uint4 *>(ref + (cwA + 1) * (int64_t)P.k) + g);
+    }
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(smw + c * 2 * Z + j);
+    uint32_t ha[4], hb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 w = w4[q];
+      // (-L) > 0  <=>  L < 0 (fp16, -0 excluded): mask halves
+      const uint32_t m0 = __hlt2_mask(u2h(w.x), u2h(0u)), m1 = __hlt2_mask(u2h(w.y), u2h(0u));
+      const uint32_t m2 = __hlt2_mask(u2h(w.z), u2h(0u)), m3 = __hlt2_mask(u2h(w.w), u2h(0u));
+      ha[q] = (m0 & 1u) | ((m1 & 1u) << 8) | ((m2 & 1u) << 16) | ((m3 & 1u) << 24);
+      hb[q] = ((m0 >> 16) & 1u) | ((m1 >> 8) & 0x100u) | (m2 & 0x10000u) | ((m3 << 8) & 0x1000000u);
+    }
+    if (hard_k) {
+      reinterpret_cast<uint4 *>(hard_k + cwA * (int64_t)P.k)[g] = make_uint4(ha[0], ha[1], ha[2], ha[3]);
+      if (hasB) reinterpret_cast<uint4 *>(hard_k + (cwA + 1) * (int64_t)P.k)[g] = make_uint4(hb[0], hb[1], hb[2], hb[3]);
+    }
+    errA += __popc(ha[0] ^ rA.x) + __popc(ha[1] ^ rA.y) + __popc(ha[2] ^ rA.z) + __popc(ha[3] ^ rA.w);
+    errB += __popc(hb[0] ^ rB.x) + __popc(hb[1] ^ rB.y) + __popc(hb[2] ^ rB.z) + __popc(hb[3] ^ rB.w);
+  }
+  if (ref && counts) {
+    h2w_count(errA, counts, red, t, NT);
+    if (hasB) h2w_count(errB, counts, red, t, NT);
+  }
 }
 
 // channel words of VN v for codewords A / B, no repetition (n <= buffer):
@@ -590,6 +698,9 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   const __half2 al2 = __float2half2_rn(alpha);
   const bool scaled = alpha != 1.0f;
   const bool norep = P.n <= P.buflen && !(dbg & 1);
+  // 16 hard decisions per thread with 128-bit loads / stores
+  const bool vec_emit = P.k % 16 == 0 && Z % 16 == 0 && !(dbg & 2);
+  const bool vec_init = norep && Z % 4 == 0 && P.k % 4 == 0 && P.k_full % 4 == 0 && P.n % 4 == 0 && !(dbg & 4);
   const int64_t npairs = (batch + 1) / 2;
   const char *base = reinterpret_cast<const char *>(smw);
   // channel word w of VN v into the layout: C (extension columns twice) and
@@ -607,12 +718,18 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     }
   };
   auto prefetch_pair = [&](int64_t pr) {
-    if (pr >= npairs || (dbg & 2)) return;
+    if (pr >= npairs) return;
     const int64_t cw0 = 2 * pr;
     const int64_t bytes = 4 * (int64_t)P.n * (cw0 + 1 < batch ? 2 : 1);
     const char *row = reinterpret_cast<const char *>(llr + cw0 * (int64_t)P.n);
     for (int64_t off = 128 * (int64_t)t; off < bytes; off += 128 * (int64_t)NT)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+    if (ref) {
+      const char *rr = reinterpret_cast<const char *>(ref + cw0 * (int64_t)P.k);
+      const int64_t rb = (int64_t)P.k * (cw0 + 1 < batch ? 2 : 1);
+      for (int64_t off = 128 * (int64_t)t; off < rb; off += 128 * (int64_t)NT)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rr + off));
+    }
   };
   prefetch_pair(blockIdx.x);
   for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
@@ -620,7 +737,54 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     const bool hasB = cwB < batch;
     const float *rowA = llr + cwA * (int64_t)P.n;
     const float *rowB = hasB ? rowA + P.n : rowA;
-    if (norep) {
+    if (vec_init) {
+      // groups of 4 VNs (every region boundary is a multiple of 4): two
+      // 128-bit loads per group, 128-bit shared stores; two groups in flight
+      constexpr int NG = NVT / 4;
+      for (int g0 = t; g0 < NG; g0 += 2 * NT) {
+        float4 a[2], b[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int v = 4 * (g0 + u * NT);
+          a[u] = b[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (g0 + u * NT < NG && v >= 2 * P.z && !(v >= P.k && v < P.k_full)) {
+            const int pos = v < P.k ? v - 2 * P.z : P.l1 + (v - P.k_full);
+            if (pos < P.n) {
+              a[u] = __ldg(reinterpret_cast<const float4 *>(rowA + pos));
+              if (hasB) b[u] = __ldg(reinterpret_cast<const float4 *>(rowB + pos));
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int v = 4 * (g0 + u * NT);
+          if (g0 + u * NT >= NG) continue;
+          uint4 w;
+          if (v >= P.k && v < P.k_full) {  // fillers: mother -40
+            w.x = w.y = w.z = w.w = h2u(__float2half2_rn(40.0f));
+          } else if (v < 2 * P.z) {  // punctured: +0.0
+            const uint32_t z = h2u(__floats2half2_rn(-0.0f, hasB ? -0.0f : 40.0f));
+            w.x = w.y = w.z = w.w = z;
+          } else {  // -(0 + L), the value chan_value forms (untransmitted: -0)
+            const float nb = hasB ? 0.0f : -40.0f;
+            w.x = h2u(__floats2half2_rn(-(0.0f + a[u].x), -(nb + b[u].x)));
+            w.y = h2u(__floats2half2_rn(-(0.0f + a[u].y), -(nb + b[u].y)));
+            w.z = h2u(__floats2half2_rn(-(0.0f + a[u].z), -(nb + b[u].z)));
+            w.w = h2u(__floats2half2_rn(-(0.0f + a[u].w), -(nb + b[u].w)));
+          }
+          const int c = v / Z, j = v - c * Z;
+          if (c < NCA) {
+            reinterpret_cast<uint4 *>(C)[v / 4] = w;
+            reinterpret_cast<uint4 *>(smw + c * 2 * Z + j)[0] = w;
+            reinterpret_cast<uint4 *>(smw + c * 2 * Z + Z + j)[0] = w;
+          } else {
+            const int o = NCA * Z + (c - NCA) * 2 * Z + j;
+            reinterpret_cast<uint4 *>(C + o)[0] = w;
+            reinterpret_cast<uint4 *>(C + o + Z)[0] = w;
+          }
+        }
+      }
+    } else if (norep) {
       // four independent loads in flight per thread
       constexpr int U = 4;
       for (int v0 = t; v0 < NVT; v0 += U * NT) {
@@ -644,40 +808,31 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
     __syncthreads();
     for (int it = 0; it < num_iter; ++it) {
-      h2_cn<Geo, false, true>(st, base, h, true, al2, scaled, Geo{}, reinterpret_cast<const char *>(C));
+      if (!(dbg & 32))
+        h2_cn<Geo, false, true>(st, base, h, true, al2, scaled, Geo{}, reinterpret_cast<const char *>(C));
       __syncthreads();
-      h2w_vn<Geo>(st, smw, h, t);
+      h2w_vn<Geo>(st, smw, h, t, dbg);
     }
     // hard decisions of the systematic columns (k <= KB * Z < NCA * Z)
-    auto emit = [&](int64_t cw, int hb) {
-      if (iters_used && t == 0) iters_used[cw] = num_iter;
-      unsigned err = 0;
-      for (int v = t; v < P.k; v += NT) {
-        const int c = v / Z, j = v - c * Z;
-        const uint32_t w = smw[c * 2 * Z + j];
-        const unsigned short hv = (unsigned short)(hb ? (w >> 16) : (w & 0xFFFFu));
-        const uint8_t hd = (-__half2float(__ushort_as_half(hv))) > 0.0f;
-        if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
-        if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
-      }
-      if (ref && counts) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
-        if ((t & 31) == 0) red[t >> 5] = err;
-        __syncthreads();
-        if (t == 0) {
-          unsigned long long tt = 0;
-          for (int w = 0; w < NT / 32; ++w) tt += red[w];
-          if (tt) {
-            atomicAdd(&counts[0], tt);
-            atomicAdd(&counts[1], 1ULL);
-          }
+    if (vec_emit) {
+      h2w_emit_vec<Geo>(P, smw, cwA, hasB, num_iter, hard_k, iters_used, ref, counts, red, t);
+    } else {
+      auto emit = [&](int64_t cw, int hb) {
+        if (iters_used && t == 0) iters_used[cw] = num_iter;
+        unsigned err = 0;
+        for (int v = t; v < P.k; v += NT) {
+          const int c = v / Z, j = v - c * Z;
+          const uint32_t w = smw[c * 2 * Z + j];
+          const unsigned short hv = (unsigned short)(hb ? (w >> 16) : (w & 0xFFFFu));
+          const uint8_t hd = (-__half2float(__ushort_as_half(hv))) > 0.0f;
+          if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
+          if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
         }
-        __syncthreads();  // red[] is reused by the next emit
-      }
-    };
-    emit(cwA, 0);
-    if (hasB) emit(cwB, 1);
+        if (ref && counts) h2w_count(err, counts, red, t, NT);
+      };
+      emit(cwA, 0);
+      if (hasB) emit(cwB, 1);
+    }
     __syncthreads();  // the next pair's channel words overwrite T
   }
 }
@@ -868,6 +1023,28 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
 }
 
+// persistent wrap-free fixed-iteration decoder: one CTA per SM (or as many
+// as fit), each walking codeword pairs
+template <class W>
+int launch_h2w(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, uint8_t *hard_k,
+               int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s, int dbg) {
+  auto kern = k_qc_fast_h2w<W>;
+  // the 128-bit paths need aligned rows (dbg bits 2 / 4 turn them off)
+  if (((uintptr_t)hard_k | (uintptr_t)ref) & 15) dbg |= 2;
+  if ((uintptr_t)llr & 15) dbg |= 4;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::nt(), W::SMEM);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
+  if (grid > 0)
+    kern<<<(unsigned)grid, W::nt(), W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, dbg);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+}
+
 // specialised instance (qc_instances.h)
 template <class G, int Z, int R, int SPLIT>
 int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
@@ -880,19 +1057,8 @@ int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int nu
   if constexpr (W::FITS && Z % 32 == 0 && R > 4) {
     const char *env = getenv("LSB_H2_WRAPFREE");
     if (!early_stop && !llr_out && S::CHN_SMEM && !(env && env[0] == '0')) {
-      auto kern = k_qc_fast_h2w<W>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
-      if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
-      int dev = 0, sms = 148, per_sm = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::NT, W::SMEM);
-      const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
-      if (grid > 0)
-        kern<<<(unsigned)grid, S::NT, W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts,
-                                                    env ? atoi(env) >> 1 : 0);
-      e = cudaGetLastError();
-      return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+      const int dbg = env ? atoi(env) >> 1 : 0;
+      return launch_h2w<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s, dbg);
     }
   }
   return launch_h2(H2GeoCT<G, Z, R, SPLIT>{}, S::NT, S::SMEM, S::CHN_SMEM, P, llr, B, num_iter, alpha, early_stop,
