@@ -837,6 +837,81 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   }
 }
 
+// hard decisions of one codeword (half hb of the posterior words tot[v]),
+// 16 per thread: four 128-bit shared loads, one 128-bit store, the reference
+// bits compared with one 128-bit load (k % 16 == 0, 16-byte aligned rows)
+__device__ __forceinline__ void h2_emit_vec1(const QcChanParams &P, const uint32_t *tot, int64_t cw, int hb, int used,
+                                             uint8_t *hard_k, int32_t *iters_used, const uint8_t *ref,
+                                             unsigned long long *counts, unsigned *red, int t, int NT) {
+  if (iters_used && t == 0) iters_used[cw] = used;
+  unsigned err = 0;
+  for (int g = t; g < P.k / 16; g += NT) {
+    uint4 r = make_uint4(0u, 0u, 0u, 0u);
+    if (ref) r = __ldg(reinterpret_cast<const uint4 *>(ref + cw * (int64_t)P.k) + g);
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(tot + 16 * g);
+    uint32_t hv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 w = w4[q];
+      uint32_t m0 = __hlt2_mask(u2h(w.x), u2h(0u)), m1 = __hlt2_mask(u2h(w.y), u2h(0u));
+      uint32_t m2 = __hlt2_mask(u2h(w.z), u2h(0u)), m3 = __hlt2_mask(u2h(w.w), u2h(0u));
+      if (hb) {
+        m0 >>= 16;
+        m1 >>= 16;
+        m2 >>= 16;
+        m3 >>= 16;
+      }
+      hv[q] = (m0 & 1u) | ((m1 & 1u) << 8) | ((m2 & 1u) << 16) | ((m3 & 1u) << 24);
+    }
+    if (hard_k) reinterpret_cast<uint4 *>(hard_k + cw * (int64_t)P.k)[g] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    err += __popc(hv[0] ^ r.x) + __popc(hv[1] ^ r.y) + __popc(hv[2] ^ r.z) + __popc(hv[3] ^ r.w);
+  }
+  if (ref && counts) h2w_count(err, counts, red, t, NT);
+}
+
+// channel words of one codeword into half q of the cached channel and
+// posterior words, four VNs per 128-bit load (every region boundary a
+// multiple of 4, no repetition, 16-byte aligned rows); the value chan_value
+// forms
+__device__ __forceinline__ void h2_refill_half_vec(const QcChanParams &P, const float *row, int q,
+                                                   unsigned short *c16, unsigned short *t16, int NV, int t, int NT) {
+  const int NG = NV / 4;
+  for (int g0 = t; g0 < NG; g0 += 2 * NT) {
+    float4 a[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int v = 4 * (g0 + u * NT);
+      a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g0 + u * NT < NG && v >= 2 * P.z && !(v >= P.k && v < P.k_full)) {
+        const int pos = v < P.k ? v - 2 * P.z : P.l1 + (v - P.k_full);
+        if (pos < P.n) a[u] = __ldg(reinterpret_cast<const float4 *>(row + pos));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int v = 4 * (g0 + u * NT);
+      if (g0 + u * NT >= NG) continue;
+      float f[4];
+      if (v >= P.k && v < P.k_full) {
+        f[0] = f[1] = f[2] = f[3] = 40.0f;
+      } else if (v < 2 * P.z) {
+        f[0] = f[1] = f[2] = f[3] = -0.0f;
+      } else {
+        f[0] = -(0.0f + a[u].x);
+        f[1] = -(0.0f + a[u].y);
+        f[2] = -(0.0f + a[u].z);
+        f[3] = -(0.0f + a[u].w);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const unsigned short hv = __half_as_ushort(__float2half_rn(f[e]));
+        c16[2 * (v + e) + q] = hv;
+        t16[2 * (v + e) + q] = hv;
+      }
+    }
+  }
+}
+
 // zero the check state of the refilled half(s): every state word keeps
 // codeword A in its low and B in its high half
 template <class Geo>
@@ -874,7 +949,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     k_qc_fast_h2p(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int64_t batch, int num_iter,
                   float alpha, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
                   int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
-                  unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next) {
+                  unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next, int vec) {
   constexpr int SPLIT = Geo::SPLIT;
   extern __shared__ uint32_t smw[];
   const int NV = geo.nv(), NT = geo.nt();
@@ -930,6 +1005,10 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
       const char *row = reinterpret_cast<const char *>(llr + pend * (int64_t)P.n);
       for (int64_t off = 128 * (int64_t)t; off < 4 * (int64_t)P.n; off += 128 * (int64_t)NT)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+      if (ref) {
+        const char *rr = reinterpret_cast<const char *>(ref + pend * (int64_t)P.k);
+        for (int off = 128 * t; off < P.k; off += 128 * NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(rr + off));
+      }
     }
     if (new0 | new1) {
       unsigned short *c16 = reinterpret_cast<unsigned short *>(chn);
@@ -937,10 +1016,14 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
       for (int q = 0; q < 2; ++q) {
         if (!(q ? new1 : new0)) continue;
         const float *row = llr + (q ? cw1 : cw0) * (int64_t)P.n;
-        for (int v = t; v < NV; v += NT) {
-          const unsigned short hv = __half_as_ushort(__float2half_rn(chan_value(P, row, v)));
-          c16[2 * v + q] = hv;
-          t16[2 * v + q] = hv;
+        if (vec & 1) {
+          h2_refill_half_vec(P, row, q, c16, t16, NV, t, NT);
+        } else {
+          for (int v = t; v < NV; v += NT) {
+            const unsigned short hv = __half_as_ushort(__float2half_rn(chan_value(P, row, v)));
+            c16[2 * v + q] = hv;
+            t16[2 * v + q] = hv;
+          }
         }
       }
       // fresh check state for the refilled half (the other half continues)
@@ -959,8 +1042,11 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
       const int itq = slot_it[q];
       const bool conv = itq > 0 && !(q ? bad1 : bad0);
       if (conv || itq == num_iter) {
-        h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cw, llr + cw * (int64_t)P.n, q, itq, hard_k, llr_out, iters_used, ref,
-                             counts, red);
+        if (vec & 2)
+          h2_emit_vec1(P, tot, cw, q, itq, hard_k, iters_used, ref, counts, red, t, NT);
+        else
+          h2_emit<Geo::NT_MAX>(P, tot, NV, NT, cw, llr + cw * (int64_t)P.n, q, itq, hard_k, llr_out, iters_used,
+                               ref, counts, red);
         __syncthreads();
         if (t == 0) slot_cw[q] = -1;
         freed = true;
@@ -999,8 +1085,17 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
     e = cudaMallocAsync((void **)&next, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(counter)");
     cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+    // 128-bit refill (bit 0) / hard-decision emit (bit 1) where the geometry
+    // and the row alignment allow
+    int vec = 0;
+    if (P.z % 4 == 0 && P.k % 4 == 0 && P.k_full % 4 == 0 && P.n % 4 == 0 && P.n <= P.buflen &&
+        !((uintptr_t)llr & 15))
+      vec |= 1;
+    if (!llr_out && P.k % 16 == 0 && !(((uintptr_t)hard_k | (uintptr_t)ref) & 15)) vec |= 2;
+    const char *env = getenv("LSB_H2_WRAPFREE");
+    if (env && env[0] == '0') vec = 0;
     kp<<<(unsigned)grid, nt, smem, s>>>(P, geo, llr, B, num_iter, alpha, hard_k, llr_out, iters_used, ref, counts,
-                                        next);
+                                        next, vec);
     e = cudaGetLastError();
     cudaFreeAsync(next, s);
     return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
