@@ -842,13 +842,21 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
 // bits compared with one 128-bit load (k % 16 == 0, 16-byte aligned rows)
 __device__ __forceinline__ void h2_emit_vec1(const QcChanParams &P, const uint32_t *tot, int64_t cw, int hb, int used,
                                              uint8_t *hard_k, int32_t *iters_used, const uint8_t *ref,
-                                             unsigned long long *counts, unsigned *red, int t, int NT) {
+                                             unsigned long long *counts, unsigned *red, int t, int NT,
+                                             int colstride = 0) {
   if (iters_used && t == 0) iters_used[cw] = used;
   unsigned err = 0;
   for (int g = t; g < P.k / 16; g += NT) {
     uint4 r = make_uint4(0u, 0u, 0u, 0u);
     if (ref) r = __ldg(reinterpret_cast<const uint4 *>(ref + cw * (int64_t)P.k) + g);
-    const uint4 *w4 = reinterpret_cast<const uint4 *>(tot + 16 * g);
+    // posterior word of VN v: tot[v], or tot[(v / Z) * colstride + v % Z]
+    // (16 | Z) in the wrap-free layout
+    int wi = 16 * g;
+    if (colstride) {
+      const int c = wi / P.z;
+      wi = c * colstride + (wi - c * P.z);
+    }
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(tot + wi);
     uint32_t hv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1064,6 +1072,169 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
   }
 }
 
+
+// Persistent early-stop decoder on the wrap-free layout (H2GeoCTW): the slot
+// refilling of k_qc_fast_h2p with the check-node reads, first-touch
+// accumulation and combine of k_qc_fast_h2w.  Hard decisions and counts only
+// (no posterior output); bit-identical to k_qc_fast_h2p<H2GeoCT, true>.
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT_MAX, 1)
+    k_qc_fast_h2pw(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
+                   uint8_t *__restrict__ hard_k, int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
+                   unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next, int vec) {
+  constexpr int Z = Geo::z(), NCA = Geo::NCA, NCD = Geo::NCD, NT = Geo::nt(), NVT = (NCA + NCD) * Z;
+  extern __shared__ uint32_t smw[];
+  uint32_t *C = smw + Geo::C_OFF;
+  __shared__ unsigned red[Geo::NT_MAX / 32];
+  __shared__ long long slot_cw[2], pend;
+  __shared__ int slot_it[2], slot_new[2], pend_new;
+  const int t = threadIdx.x;
+  const int h = t / Geo::nt1();
+  const char *base = reinterpret_cast<const char *>(smw);
+  const __half2 al2 = __float2half2_rn(alpha);
+  const bool scaled = alpha != 1.0f;
+  H2State<Geo::NR> st;
+#pragma unroll
+  for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
+  auto claim = [&]() -> long long {
+    const unsigned long long c = atomicAdd(next, 1ULL);
+    return (long long)c < batch ? (long long)c : -1;
+  };
+  if (t == 0) {
+    slot_cw[0] = slot_cw[1] = -1;
+    slot_it[0] = slot_it[1] = 0;
+    pend = claim();
+  }
+  __syncthreads();
+  unsigned short *c16 = reinterpret_cast<unsigned short *>(C);
+  unsigned short *t16 = reinterpret_cast<unsigned short *>(smw);
+  // half q of VN v's channel word into the layout (C, extension columns
+  // twice, and both copies of T)
+  auto put16 = [&](int v, int q, unsigned short hv) {
+    const int c = v / Z, j = v - c * Z;
+    if (c < NCA) {
+      c16[2 * v + q] = hv;
+      t16[2 * (c * 2 * Z + j) + q] = hv;
+      t16[2 * (c * 2 * Z + Z + j) + q] = hv;
+    } else {
+      const int o = NCA * Z + (c - NCA) * 2 * Z + j;
+      c16[2 * o + q] = hv;
+      c16[2 * (o + Z) + q] = hv;
+    }
+  };
+  for (;;) {
+    if (t == 0) {
+      pend_new = 0;
+      for (int q = 0; q < 2; ++q) {
+        slot_new[q] = 0;
+        if (slot_cw[q] < 0 && pend >= 0) {
+          slot_cw[q] = pend;
+          slot_it[q] = 0;
+          slot_new[q] = 1;
+          pend = claim();
+          pend_new = 1;
+        }
+      }
+    }
+    __syncthreads();
+    const long long cw0 = slot_cw[0], cw1 = slot_cw[1];
+    if (cw0 < 0 && cw1 < 0) return;
+    const int new0 = slot_new[0], new1 = slot_new[1];
+    if (pend_new && pend >= 0) {
+      const char *row = reinterpret_cast<const char *>(llr + pend * (int64_t)P.n);
+      for (int64_t off = 128 * (int64_t)t; off < 4 * (int64_t)P.n; off += 128 * (int64_t)NT)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+      if (ref) {
+        const char *rr = reinterpret_cast<const char *>(ref + pend * (int64_t)P.k);
+        for (int off = 128 * t; off < P.k; off += 128 * NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(rr + off));
+      }
+    }
+    if (new0 | new1) {
+      for (int q = 0; q < 2; ++q) {
+        if (!(q ? new1 : new0)) continue;
+        const float *row = llr + (q ? cw1 : cw0) * (int64_t)P.n;
+        if (vec & 1) {
+          constexpr int NG = NVT / 4;
+          for (int g0 = t; g0 < NG; g0 += 2 * NT) {
+            float4 a[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int v = 4 * (g0 + u * NT);
+              a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (g0 + u * NT < NG && v >= 2 * P.z && !(v >= P.k && v < P.k_full)) {
+                const int pos = v < P.k ? v - 2 * P.z : P.l1 + (v - P.k_full);
+                if (pos < P.n) a[u] = __ldg(reinterpret_cast<const float4 *>(row + pos));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int v = 4 * (g0 + u * NT);
+              if (g0 + u * NT >= NG) continue;
+              float f[4];
+              if (v >= P.k && v < P.k_full) {
+                f[0] = f[1] = f[2] = f[3] = 40.0f;
+              } else if (v < 2 * P.z) {
+                f[0] = f[1] = f[2] = f[3] = -0.0f;
+              } else {
+                f[0] = -(0.0f + a[u].x);
+                f[1] = -(0.0f + a[u].y);
+                f[2] = -(0.0f + a[u].z);
+                f[3] = -(0.0f + a[u].w);
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) put16(v + e, q, __half_as_ushort(__float2half_rn(f[e])));
+            }
+          }
+        } else {
+          for (int v = t; v < NVT; v += NT) put16(v, q, __half_as_ushort(__float2half_rn(chan_value(P, row, v))));
+        }
+      }
+      h2_reset_half<Geo>(st, h, new0, new1);
+      __syncthreads();
+    }
+    const uint32_t synx = h2_cn<Geo, true, true>(st, base, h, true, al2, scaled, Geo{},
+                                                 reinterpret_cast<const char *>(C));
+    const int bad0 = __syncthreads_or((synx >> 15) & 1u);
+    const int bad1 = __syncthreads_or(synx >> 31);
+    bool freed = false;
+    for (int q = 0; q < 2; ++q) {
+      const long long cw = q ? cw1 : cw0;
+      if (cw < 0) continue;
+      const int itq = slot_it[q];
+      const bool conv = itq > 0 && !(q ? bad1 : bad0);
+      if (conv || itq == num_iter) {
+        if (vec & 2) {
+          h2_emit_vec1(P, smw, cw, q, itq, hard_k, iters_used, ref, counts, red, t, NT, 2 * Z);
+        } else {
+          if (iters_used && t == 0) iters_used[cw] = itq;
+          unsigned err = 0;
+          for (int v = t; v < P.k; v += NT) {
+            const int c = v / Z, j = v - c * Z;
+            const uint32_t w = smw[c * 2 * Z + j];
+            const unsigned short hv = (unsigned short)(q ? (w >> 16) : (w & 0xFFFFu));
+            const uint8_t hd = (-__half2float(__ushort_as_half(hv))) > 0.0f;
+            if (hard_k) hard_k[cw * (int64_t)P.k + v] = hd;
+            if (ref) err += (hd != ref[cw * (int64_t)P.k + v]);
+          }
+          if (ref && counts) h2w_count(err, counts, red, t, NT);
+        }
+        __syncthreads();
+        if (t == 0) slot_cw[q] = -1;
+        freed = true;
+      }
+    }
+    if (freed) {
+      __syncthreads();
+      if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
+    }
+    h2w_vn<Geo>(st, smw, h, t);
+    if (t == 0) {
+      slot_it[0] += 1;
+      slot_it[1] += 1;
+    }
+  }
+}
+
 // launch either kernel for a geometry with `nt` threads and `smem` bytes of
 // dynamic shared memory; the persistent one when early stopping and the
 // channel LLRs fit in shared memory
@@ -1140,6 +1311,32 @@ int launch_h2w(const QcChanParams &P, const float *llr, int64_t B, int num_iter,
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
 }
 
+// persistent early-stop decoder on the wrap-free layout
+template <class W>
+int launch_h2pw(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, uint8_t *hard_k,
+                int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
+  auto kern = k_qc_fast_h2pw<W>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::nt(), W::SMEM);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
+  int vec = 0;
+  if (P.k % 4 == 0 && P.k_full % 4 == 0 && P.n % 4 == 0 && P.n <= P.buflen && !((uintptr_t)llr & 15)) vec |= 1;
+  if (P.k % 16 == 0 && W::z() % 16 == 0 && !(((uintptr_t)hard_k | (uintptr_t)ref) & 15)) vec |= 2;
+  unsigned long long *next = nullptr;
+  e = cudaMallocAsync((void **)&next, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(counter)");
+  cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+  kern<<<(unsigned)grid, W::nt(), W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, next,
+                                                 vec);
+  e = cudaGetLastError();
+  cudaFreeAsync(next, s);
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+}
+
 // specialised instance (qc_instances.h)
 template <class G, int Z, int R, int SPLIT>
 int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
@@ -1155,6 +1352,8 @@ int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int nu
       const int dbg = env ? atoi(env) >> 1 : 0;
       return launch_h2w<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s, dbg);
     }
+    if (early_stop && !llr_out && S::CHN_SMEM && B >= 4 && !(env && env[0] == '0'))
+      return launch_h2pw<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s);
   }
   return launch_h2(H2GeoCT<G, Z, R, SPLIT>{}, S::NT, S::SMEM, S::CHN_SMEM, P, llr, B, num_iter, alpha, early_stop,
                    hard_k, llr_out, iters_used, ref, counts, s);

@@ -451,21 +451,24 @@ def test_fp16x2_runtime_geometry_equals_specialised_instance():
 @pytest.mark.parametrize("k,n,m,ebno", [(8448, 16896, 4, 5.8), (4096, 8192, 2, 3.0), (2816, 5632, 2, 3.0),
                                         (704, 1408, 2, 3.0), (4096, 12288, 6, 7.0)])
 def test_wrap_free_layout_equals_wrapped_kernel(k, n, m, ebno, monkeypatch):
-    """The fixed-iteration wrap-free kernel (doubled posterior columns, no
-    modulo in the check-node reads) runs the wrapped kernel's arithmetic in
-    the same order: bit-identical hard decisions and fused counts, odd batch
-    included (the last CTA has one codeword)."""
+    """The wrap-free kernels (doubled posterior columns, no modulo in the
+    check-node reads; fixed-iteration and persistent early-stop) run the
+    wrapped kernels' arithmetic in the same order: bit-identical hard
+    decisions, fused counts and iteration counts, odd batch included."""
     bits, llr = _oracle_llrs(k, n, m, ebno, 13, 5)
     code = lb.LdpcCode5G(k, n)
     out = {}
     for wf in ("1", "0"):
         monkeypatch.setenv("LSB_H2_WRAPFREE", wf)
         for variant in ("min-sum", "scaled-min-sum"):
-            r = lb.qc_decode(llr, code, 20, variant, 0.75, early_stop=False, ref_bits=bits, precision="fp16x2")
-            out[wf, variant] = (r["hard"].cpu().numpy(), r["counts"].cpu().numpy())
+            for es in (False, True):
+                r = lb.qc_decode(llr, code, 20, variant, 0.75, early_stop=es, ref_bits=bits, want_iters=True,
+                                 precision="fp16x2")
+                out[wf, variant, es] = [r[x].cpu().numpy() for x in ("hard", "counts", "iters")]
     for variant in ("min-sum", "scaled-min-sum"):
-        a, b = out["1", variant], out["0", variant]
-        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), variant
+        for es in (False, True):
+            a, b = out["1", variant, es], out["0", variant, es]
+            assert all(np.array_equal(x, y) for x, y in zip(a, b)), (variant, es)
 
 
 @pytest.mark.parametrize("k,n,m,ebno", [(792, 1584, 2, 2.5), (200, 600, 2, 3.0), (3520, 5280, 4, 6.0),
