@@ -273,14 +273,14 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
             x = u2h(cw);
             if constexpr (SYN) {  // the unformed posterior's sign: channel + own message
               const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-              hs ^= h2u(__hadd2(u2h(cw), u2h(mag | old_sign<p>(osg, osg2))));
+              hs ^= h2u(__hadd2(u2h(cw), u2h(mag ^ old_sign<p>(osg, osg2))));
             }
           } else {
             const uint32_t tw = *reinterpret_cast<const uint32_t *>(base + geo.template off<e>(i4));
             if constexpr (SYN) hs ^= tw;
             const __half2 pp = u2h(h2_int<p>());
             const uint32_t mag = h2u(__hfma2(__heq2(oix, pp), od, o1));
-            x = __hsub2(u2h(tw), u2h(mag | old_sign<p>(osg, osg2)));
+            x = __hsub2(u2h(tw), u2h(mag ^ old_sign<p>(osg, osg2)));
           }
           const uint32_t xw = h2u(x);
           const __half2 a = __habs2(x);
@@ -304,25 +304,30 @@ __device__ __forceinline__ uint32_t h2_cn(H2State<Geo::NR> &st, const char *base
           }
           acc_sign<p>(sg, sg2, xw);
         });
-        constexpr uint32_t dm = (1u << (d < 16 ? d : 16)) - 1u;
+        // The outgoing sign of edge p is (its v2c sign) XOR (row parity): the
+        // raw v2c signs are stored and the parity rides in the sign bits of
+        // M1 and M2 - M1 (both halves), so reconstruction is
+        // fma(eq, D, M1) ^ raw sign -- one parity computation per row, no
+        // per-row flip of the sign words.
+        uint32_t pa, pb;
         if constexpr (packed) {
-          const uint32_t pa = __popc(sg & 0xFFFFu) & 1u, pb = __popc(sg >> 16) & 1u;
-          st.SG[j] = sg ^ (((0u - pa) & dm) | ((0u - pb) & (dm << 16)));
+          pa = __popc(sg & 0xFFFFu);
+          pb = __popc(sg >> 16);
         } else {
-          constexpr uint32_t dm2 = (1u << (d - 16)) - 1u;
-          const uint32_t pa = (__popc(sg & 0xFFFFu) + __popc(sg2 & 0xFFFFu)) & 1u;
-          const uint32_t pb = (__popc(sg >> 16) + __popc(sg2 >> 16)) & 1u;
-          st.SG[j] = sg ^ (((0u - pa) & dm) | ((0u - pb) & (dm << 16)));
-          st.SG2[j] = sg2 ^ (((0u - pa) & dm2) | ((0u - pb) & (dm2 << 16)));
+          pa = __popc(sg & 0xFFFFu) + __popc(sg2 & 0xFFFFu);
+          pb = __popc(sg >> 16) + __popc(sg2 >> 16);
         }
+        const uint32_t par = ((pa << 15) & 0x8000u) | (pb << 31);
+        st.SG[j] = sg;
+        if constexpr (!packed) st.SG2[j] = sg2;
         if (scaled) {
           n1 = h2u(__hmul2(u2h(n1), al2));
           n2 = h2u(__hmul2(u2h(n2), al2));
         }
         // state keeps min1 and the fp16 difference min2 - min1; the argmin
         // edge is reconstructed as min1 + diff (within 1 ulp of min2)
-        st.M1[j] = n1;
-        st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1)));
+        st.M1[j] = n1 | par;
+        st.M2[j] = h2u(__hsub2(u2h(n2), u2h(n1))) | par;
         st.IX[j] = d > 1 ? h2u(__hadd2(wv, u2h(h2_int<d - 1>()))) : 0u;
         if constexpr (SYN) synx |= hs;
       }
@@ -381,7 +386,7 @@ __device__ __forceinline__ void h2_vn(const H2State<Geo::NR> &st, uint32_t *tot,
             if constexpr (D1 && col_deg1<G, e>()) return;
             uint32_t *tp = reinterpret_cast<uint32_t *>(arr + geo.template off<e>(i4));
             const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-            *tp = h2u(__hadd2(u2h(*tp), u2h(mag | old_sign<p>(osg, osg2))));
+            *tp = h2u(__hadd2(u2h(*tp), u2h(mag ^ old_sign<p>(osg, osg2))));
           });
         }
       }
@@ -556,7 +561,7 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
           const unsigned lo4 = S4 == 0 ? i4 : min(i4 + S4, i4 + (S4 - 4u * Z));  // 4 * ((i + s) mod Z)
           uint32_t *tp = reinterpret_cast<uint32_t *>(arr + 4u * Geo::acc_word(H, (int)c) + lo4);
           const uint32_t mag = h2u(__hfma2(__heq2(oix, u2h(h2_int<p>())), od, o1));
-          const __half2 msg = u2h(mag | old_sign<p>(osg, osg2));
+          const __half2 msg = u2h(mag ^ old_sign<p>(osg, osg2));
           constexpr bool first = h2w_first_step<G, SPLIT, Geo::RB>(H, (int)c) == j;
           if constexpr (!first) {
             *tp = h2u(__hadd2(u2h(*tp), msg));
