@@ -690,7 +690,7 @@ __device__ __forceinline__ uint32_t chan_word_norep(const QcChanParams &P, const
 // so the load at the start of a pair hits L2.  Hard decisions and counts
 // only (no posterior output).
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT_MAX, 1)
+__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_fast_h2w(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
                   uint8_t *__restrict__ hard_k, int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
                   unsigned long long *__restrict__ counts, int dbg) {
@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
 // accumulation and combine of k_qc_fast_h2w.  Hard decisions and counts only
 // (no posterior output); bit-identical to k_qc_fast_h2p<H2GeoCT, true>.
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT_MAX, 1)
+__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_fast_h2pw(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
                    uint8_t *__restrict__ hard_k, int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
                    unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next, int vec) {
