@@ -577,8 +577,7 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
     });
   });
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
-  if (!(dbg & 16)) for (int v = t; v < NQ; v += NT) {
-    const int c = v / Z4, j = v - c * Z4;
+  auto combine = [&](int c, int j) {
     uint4 x = S4w[c * 2 * Z4 + j];
 #pragma unroll
     for (int q = 1; q < SPLIT; ++q) {
@@ -594,6 +593,20 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
     x.w = h2u(__hmin2(__hmax2(u2h(x.w), lo), hi));
     S4w[c * 2 * Z4 + j] = x;
     S4w[c * 2 * Z4 + Z4 + j] = x;
+  };
+  if (!(dbg & 16)) {
+    if constexpr (NT % Z4 == 0) {
+      // fixed (column, word) walk: no division per element
+      constexpr int CS = NT / Z4;  // columns per sweep
+      const int c0 = t / Z4, j = t - c0 * Z4;
+#pragma unroll
+      for (int c = c0; c < NCA; c += CS) combine(c, j);
+    } else {
+      for (int v = t; v < NQ; v += NT) {
+        const int c = v / Z4;
+        combine(c, v - c * Z4);
+      }
+    }
   }
   __syncthreads();
 }
