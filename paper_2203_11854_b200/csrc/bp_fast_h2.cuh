@@ -573,9 +573,12 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
           }
         });
       }
-      __syncthreads();
+      // the slots accumulate into disjoint arrays: each slot only waits for
+      // its own warps between row steps (named barrier 1 + H)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + H), "r"(Geo::nt1()) : "memory");
     });
   });
+  __syncthreads();
   const __half2 lo = __float2half2_rn(-40.0f), hi = __float2half2_rn(40.0f);
   auto combine = [&](int c, int j) {
     uint4 x = S4w[c * 2 * Z4 + j];
