@@ -500,6 +500,34 @@ __host__ __device__ constexpr int h2w_first_step(int q, int c) {
   return -1;
 }
 
+// true when rows r1 and r2 share an accumulated (non-degree-1) column
+template <class G>
+__host__ __device__ constexpr bool h2w_rows_overlap(int r1, int r2) {
+  for (int a = G::row_start[r1]; a < G::row_start[r1 + 1]; ++a) {
+    const int c = G::col[a];
+    if (G::col_start[c + 1] - G::col_start[c] == 1) continue;
+    for (int b = G::row_start[r2]; b < G::row_start[r2 + 1]; ++b)
+      if (G::col[b] == c) return true;
+  }
+  return false;
+}
+
+// Variable-node row steps of slot q: consecutive rows j, j + 1, ... that
+// share no accumulated column run in one step (no barrier between them;
+// every variable still receives its messages in row order).  True when slot
+// q needs a barrier after its row j.
+template <class G, int SPLIT, int RB>
+__host__ __device__ constexpr bool h2w_step_ends(int q, int j) {
+  const int r = j * SPLIT + q, rn = r + SPLIT;
+  if (rn >= RB) return true;
+  // the group holding row j starts at the last barrier before it
+  int j0 = j;
+  while (j0 > 0 && !h2w_step_ends<G, SPLIT, RB>(q, j0 - 1)) --j0;
+  for (int jj = j0; jj <= j; ++jj)
+    if (h2w_rows_overlap<G>(jj * SPLIT + q, rn)) return true;
+  return false;
+}
+
 // Variable-node phase of the wrap-free layout (H2GeoCTW): posteriors =
 // clip(chan + sum of the new messages) over the NCA accumulated columns,
 // written to both copies of each column.  Both copies of T are dead once the
@@ -574,8 +602,10 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
         });
       }
       // the slots accumulate into disjoint arrays: each slot only waits for
-      // its own warps between row steps (named barrier 1 + H)
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + H), "r"(Geo::nt1()) : "memory");
+      // its own warps between row steps (named barrier 1 + H), and not at all
+      // between consecutive rows that share no accumulated column
+      if constexpr (h2w_step_ends<G, SPLIT, Geo::RB>(H, j))
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + H), "r"(Geo::nt1()) : "memory");
     });
   });
   __syncthreads();
