@@ -265,7 +265,7 @@ def run_b200(a, rank, world, local_rank):
                          # DRAM bytes per launch: ncu --set full capture of k_qc_fast_h2 on 2368
                          # codewords (184.3 MB read+write, profiles/r01/ncu_k_qc_fast_h2_v5_*), scaled to this batch;
                          # the messages never leave the SM, DRAM sees the LLR input only
-                         "traffic": (B * 188_144_384 / 2368) if pipe.precision == "fp16x2" else None,
+                         "traffic": (B * 184_333_312 / 2368) if pipe.precision == "fp16x2" else None,
                          "kernel": "k_qc_fast_h2w" if pipe.precision == "fp16x2" else "k_qc_fast2",
                          "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
                          "kernel_ms_per_launch": per_launch_ms,
