@@ -535,7 +535,7 @@ __host__ __device__ constexpr bool h2w_step_ends(int q, int j) {
 // into its second copy and slot q >= 2 into A[q-2] (Geo::acc_word); these
 // writes wrap (i + s) mod Z as usual.
 template <class Geo>
-__device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw, int h, int t, int dbg = 0) {
+__device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw, int h, int t) {
   using G = typename Geo::G;
   constexpr int SPLIT = Geo::SPLIT, NR = Geo::NR, Z = Geo::z(), NCA = Geo::NCA, NT = Geo::nt();
   constexpr int Z4 = Z / 4;
@@ -568,7 +568,7 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
     });
     __syncthreads();
   }
-  if (!(dbg & 8)) sfor<0, SPLIT>([&](auto hc) {
+  sfor<0, SPLIT>([&](auto hc) {
     constexpr int H = decltype(hc)::value;
     if (h != H) return;
     const unsigned i4 = 4u * tid_volatile() - 4u * H * Geo::nt1();
@@ -627,7 +627,7 @@ __device__ __forceinline__ void h2w_vn(const H2State<Geo::NR> &st, uint32_t *smw
     S4w[c * 2 * Z4 + j] = x;
     S4w[c * 2 * Z4 + Z4 + j] = x;
   };
-  if (!(dbg & 16)) {
+  {
     if constexpr (NT % Z4 == 0) {
       // fixed (column, word) walk: no division per element
       constexpr int CS = NT / Z4;  // columns per sweep
@@ -739,7 +739,7 @@ template <class Geo>
 __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     k_qc_fast_h2w(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, float alpha,
                   uint8_t *__restrict__ hard_k, int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
-                  unsigned long long *__restrict__ counts, int dbg) {
+                  unsigned long long *__restrict__ counts, int paths) {
   constexpr int Z = Geo::z(), NCA = Geo::NCA, NCD = Geo::NCD, NT = Geo::nt(), NVT = (NCA + NCD) * Z;
   extern __shared__ uint32_t smw[];
   uint32_t *C = smw + Geo::C_OFF;
@@ -748,10 +748,10 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
   const int h = t / Geo::nt1();
   const __half2 al2 = __float2half2_rn(alpha);
   const bool scaled = alpha != 1.0f;
-  const bool norep = P.n <= P.buflen && !(dbg & 1);
+  const bool norep = P.n <= P.buflen;
   // 16 hard decisions per thread with 128-bit loads / stores
-  const bool vec_emit = P.k % 16 == 0 && Z % 16 == 0 && !(dbg & 2);
-  const bool vec_init = norep && Z % 4 == 0 && P.k % 4 == 0 && P.k_full % 4 == 0 && P.n % 4 == 0 && !(dbg & 4);
+  const bool vec_emit = P.k % 16 == 0 && Z % 16 == 0 && !(paths & 2);
+  const bool vec_init = norep && Z % 4 == 0 && P.k % 4 == 0 && P.k_full % 4 == 0 && P.n % 4 == 0 && !(paths & 4);
   const int64_t npairs = (batch + 1) / 2;
   const char *base = reinterpret_cast<const char *>(smw);
   // channel word w of VN v into the layout: C (extension columns twice) and
@@ -859,10 +859,9 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     for (int j = 0; j < Geo::NR; ++j) st.M1[j] = st.M2[j] = st.IX[j] = st.SG[j] = st.SG2[j] = 0u;
     __syncthreads();
     for (int it = 0; it < num_iter; ++it) {
-      if (!(dbg & 32))
-        h2_cn<Geo, false, true>(st, base, h, true, al2, scaled, Geo{}, reinterpret_cast<const char *>(C));
+      h2_cn<Geo, false, true>(st, base, h, true, al2, scaled, Geo{}, reinterpret_cast<const char *>(C));
       __syncthreads();
-      h2w_vn<Geo>(st, smw, h, t, dbg);
+      h2w_vn<Geo>(st, smw, h, t);
     }
     // hard decisions of the systematic columns (k <= KB * Z < NCA * Z)
     if (vec_emit) {
@@ -1344,11 +1343,12 @@ int launch_h2(const Geo &geo, int nt, size_t smem, bool chn_smem, const QcChanPa
 // as fit), each walking codeword pairs
 template <class W>
 int launch_h2w(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, uint8_t *hard_k,
-               int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s, int dbg) {
+               int32_t *iters_used, const uint8_t *ref, unsigned long long *counts, cudaStream_t s) {
   auto kern = k_qc_fast_h2w<W>;
-  // the 128-bit paths need aligned rows (dbg bits 2 / 4 turn them off)
-  if (((uintptr_t)hard_k | (uintptr_t)ref) & 15) dbg |= 2;
-  if ((uintptr_t)llr & 15) dbg |= 4;
+  // the 128-bit emit (bit 2 off) and channel loads (bit 4 off) need 16-byte aligned rows
+  int paths = 0;
+  if (((uintptr_t)hard_k | (uintptr_t)ref) & 15) paths |= 2;
+  if ((uintptr_t)llr & 15) paths |= 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   int dev = 0, sms = 148, per_sm = 1;
@@ -1357,7 +1357,7 @@ int launch_h2w(const QcChanParams &P, const float *llr, int64_t B, int num_iter,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::nt(), W::SMEM);
   const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + 1) / 2);
   if (grid > 0)
-    kern<<<(unsigned)grid, W::nt(), W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, dbg);
+    kern<<<(unsigned)grid, W::nt(), W::SMEM, s>>>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, paths);
   e = cudaGetLastError();
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
 }
@@ -1400,8 +1400,7 @@ int launch_qc_fast_h2(const QcChanParams &P, const float *llr, int64_t B, int nu
   if constexpr (W::FITS && Z % 32 == 0 && R > 4) {
     const char *env = getenv("LSB_H2_WRAPFREE");
     if (!early_stop && !llr_out && S::CHN_SMEM && !(env && env[0] == '0')) {
-      const int dbg = env ? atoi(env) >> 1 : 0;
-      return launch_h2w<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s, dbg);
+      return launch_h2w<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s);
     }
     if (early_stop && !llr_out && S::CHN_SMEM && B >= 4 && !(env && env[0] == '0'))
       return launch_h2pw<W>(P, llr, B, num_iter, alpha, hard_k, iters_used, ref, counts, s);

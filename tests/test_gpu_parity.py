@@ -469,6 +469,16 @@ def test_wrap_free_layout_equals_wrapped_kernel(k, n, m, ebno, monkeypatch):
         for es in (False, True):
             a, b = out["1", variant, es], out["0", variant, es]
             assert all(np.array_equal(x, y) for x, y in zip(a, b)), (variant, es)
+    # LLR rows that are not 16-byte aligned take the scalar load path: same results
+    monkeypatch.setenv("LSB_H2_WRAPFREE", "1")
+    buf = torch.empty(llr.size + 1, dtype=torch.float32, device="cuda")
+    mis = buf[1:].view(llr.shape)
+    mis.copy_(torch.from_numpy(llr))
+    for es in (False, True):
+        r = lb.qc_decode(mis, code, 20, "min-sum", 0.75, early_stop=es, ref_bits=bits, want_iters=True,
+                         precision="fp16x2")
+        got = [r[x].cpu().numpy() for x in ("hard", "counts", "iters")]
+        assert all(np.array_equal(x, y) for x, y in zip(got, out["1", "min-sum", es])), es
 
 
 @pytest.mark.parametrize("k,n,m,ebno", [(792, 1584, 2, 2.5), (200, 600, 2, 3.0), (3520, 5280, 4, 6.0),
