@@ -108,6 +108,12 @@ struct H2GeoCTW : H2GeoCT<G_, Z, R, SPLIT_> {
   static constexpr int C_W = NCA * Z + NCD * 2 * Z;
   static constexpr size_t SMEM = 4 * (size_t)(C_OFF + C_W);
   static constexpr bool FITS = SMEM <= 225 * 1024;
+  // small lifting sizes with few rows per thread: aim for 1,024 resident
+  // threads per SM (the compact layout leaves the shared memory for it; the
+  // register cap becomes 64, enough for <= 6 rows of check state)
+  static constexpr int MINB = (H2GeoCT<G_, Z, R, SPLIT_>::NT_MAX < 768 && H2GeoCT<G_, Z, R, SPLIT_>::NR <= 6)
+                                  ? 1024 / H2GeoCT<G_, Z, R, SPLIT_>::NT_MAX
+                                  : H2GeoCT<G_, Z, R, SPLIT_>::MINB;
   template <int e>
   __device__ __forceinline__ static unsigned off(unsigned i4) {
     constexpr unsigned c = (unsigned)G_::col[e], s = (unsigned)(G_::shift[e] % Z);
