@@ -370,12 +370,17 @@ def sweep_points(cfg: SimConfig, payload_bits: int, eval_batch, dist=None, batch
 def run_sweep(cfg: SimConfig, num_workers: int = 1, batches_per_rank: int = 1) -> SweepResult:
     """Eb/N0 sweep with error-count stopping and early exit (sweep.py:411-476).
 
-    `num_workers` is accepted for signature compatibility; parallelism comes
-    from the GPU and from torch.distributed ranks (one per GPU) when
-    initialised.  Statistics are identical for any rank count.
+    As in the reference, batches run in waves of `num_workers` before each
+    stopping check (sweep.py:438-453): here a wave is enqueued on the GPU
+    without host synchronisation, `ceil(num_workers / ranks)` batches per
+    rank (or `batches_per_rank` if larger), and torch.distributed ranks (one
+    per GPU) split it.  Statistics are identical for any worker or rank
+    count (the prefix-truncation stop rule).
     """
     pipeline = build_pipeline(cfg)
     dist = _dist()
+    world = dist.get_world_size() if dist else 1
+    batches_per_rank = max(int(batches_per_rank), -(-max(1, int(num_workers)) // world))
 
     def eval_batch(snr_idx, ebno_db, bidx, out):
         rng = RngStream(cfg.seed, ((snr_idx + 1) << 32) | (bidx + 1))

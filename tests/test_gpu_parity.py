@@ -706,3 +706,20 @@ def test_run_sweep_statistics_close_to_oracle():
     bler_ref = errs / (2 * B)
     sd = np.sqrt(bler_ref * (1 - bler_ref) / (2 * B) + p.bler * (1 - p.bler) / p.blocks)
     assert abs(p.bler - bler_ref) <= 2.6 * sd + 1e-3
+
+
+def test_run_sweep_worker_count_invariance():
+    """Waves of num_workers batches (enqueued without host synchronisation)
+    give the same per-point statistics as one batch per wave, including the
+    error-count stop (reference test_acceptance.py:329-337)."""
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": 256, "n": 512, "decoder": {"variant": "min-sum", "mode": "fast"}},
+        "modulation": {"kind": "qam", "bits_per_symbol": 2},
+        "sweep": {"ebno_db": [1.0, 2.0, 3.0], "batch_size": 256, "target_block_errors": 40,
+                  "max_batches_per_point": 12}, "seed": 7})
+    key = lambda r: [(p.bits, p.bit_errors, p.blocks, p.block_errors, p.batches, p.stop_reason)  # noqa: E731
+                     for p in r.points]
+    base = key(lb.run_sweep(cfg))
+    assert any(p[5] == "target-errors" for p in base)
+    for w in (3, 8):
+        assert key(lb.run_sweep(cfg, num_workers=w)) == base, w

@@ -36,7 +36,7 @@ def config3(quick, outdir):
                       "max_batches_per_point": 20 if quick else 300},
             "seed": 2024})
         t = time.perf_counter()
-        r = lb.run_sweep(cfg)
+        r = lb.run_sweep(cfg, num_workers=8)  # waves of 8 batches, as the reference's worker pool
         torch.cuda.synchronize()
         el = time.perf_counter() - t
         csv = lb.format_csv(r)
