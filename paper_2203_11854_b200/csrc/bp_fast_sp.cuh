@@ -9,8 +9,9 @@
 // the variable update is a pure gather, total[c][j] = chan + sum over the
 // column's entries of c2v[e][(j - s_e) mod Z].
 //   CN phase (thread = lane i, row slot h): v2c = total - c2v_old,
-//            phi(x) = -log(tanh(x/2)) (ex2/rcp/lg2 MUFU, fp32, base 2), S = sum phi,
-//            c2v_new = sign * clip(phi(max(S - phi_e, 1e-12)), 0, 30)
+//            phi(x) = -log(tanh(x/2)) (fp32, base 2) kept as 2^phi (ex2/rcp MUFU),
+//            R = prod 2^phi = 2^S, 2^-(S - phi_e) = 2^phi_e / R,
+//            c2v_new = sign * clip(phi(max(S - phi_e, 1e-12)), 0, 30) (rcp/lg2 MUFU)
 //   VN phase (thread = lane j, column slot): gather + clip +-40
 // Shared memory: E_live*Z halves of messages + NCOL*Z halves of posteriors
 // (207 KB for BG1, Z=384, 24 live rows).  Channel LLRs are re-read from the
@@ -34,13 +35,11 @@ struct QcShapeSP {
 };
 
 // phi(x) = -log(tanh(x/2)) on the reference's clip range [1e-12, 40], in
-// base-2 units: sp_phi2(y) = phi(y ln2) / ln2 for y = x log2(e), so that
-// 2^-y = e^-x.  The check-node sums run in these units (the second phi then
-// needs no rescaling of its argument), and only the outgoing message is
-// converted back to natural LLR units.  phi = log2((1 + u) / (1 - u)) with
-// u = 2^-y; 1 - u comes from its Taylor series for small y (no cancellation).
-// Flush-to-zero MUFU forms (ex2, rcp, lg2: 3 MUFU, no denormal fix-ups): every
-// operand here is a normal float.
+// base-2 units: phi2(y) = phi(y ln2) / ln2 for y = x log2(e), so that
+// 2^-y = e^-x; only the outgoing message is converted back to natural LLR
+// units.  2^phi2 = (1 + u) / (1 - u) with u = 2^-y; 1 - u comes from its
+// Taylor series for small y (no cancellation).  Flush-to-zero MUFU forms (ex2,
+// rcp, lg2, no denormal fix-ups): every operand here is a normal float.
 constexpr float kPhiLo2 = 1e-12f * kLog2e, kPhiHi2 = 40.0f * kLog2e;
 
 // 1 - 2^-y without cancellation: its Taylor series for small y
@@ -50,21 +49,24 @@ __device__ __forceinline__ float sp_one_minus(float y, float u) {
   return y < 0.09f ? series : 1.0f - u;
 }
 
-// phi of the clipped argument y; also returns ratio = 2^phi = (1 + u) / (1 - u)
-__device__ __forceinline__ float sp_phi2(float y, float &ratio) {
+// Product-domain check update (k_qc_sp): the check keeps the running product
+// R = prod_e ratio_e = 2^S instead of the sum S of the per-edge phi, so the
+// first phi needs no lg2 and the check no ex2 (4 MUFU per edge instead of 5).
+// ratio of the clipped argument y: 2^phi2(y) = (1 + u) / (1 - u), u = 2^-y
+__device__ __forceinline__ float sp_ratio(float y) {
   y = fminf(fmaxf(y, kPhiLo2), kPhiHi2);
   const float u = ex2_ftz(-y);
-  ratio = (1.0f + u) * rcp_ftz(sp_one_minus(y, u));
-  return lg2_ftz(ratio);
+  return (1.0f + u) * rcp_ftz(sp_one_minus(y, u));
 }
 
-// phi(S - phi_e) for an edge of a check with S = sum of phi: the 2^-(S - phi_e)
-// it needs is 2^-S (once per check) times the edge's 2^phi_e, so the second
-// phi costs two SFU operations (rcp, lg2) instead of three
-__device__ __forceinline__ float sp_phi2_excl(float d, float e2s, float ratio) {
-  d = fmaxf(d, kPhiLo2);
-  const float u = e2s * ratio;  // = 2^-d; only used as 1 + u and, for d >= 0.09, 1 - u
-  return lg2_ftz((1.0f + u) * rcp_ftz(sp_one_minus(d, u)));
+// phi of the exclusive sum from u = 2^-(S - phi_e) = ratio_e / R.  1 - u is
+// floored at the reference's lower clip 1e-12 (ldpc.py:77-83); for a check
+// whose other edges are all very reliable (1 - u below fp32 resolution) the
+// message saturates near phi(1e-12) = 28.3 instead of its exact >= 17 value.
+// A product past the fp32 range gives u = 0 and a zero message, the fp16
+// value of the exact one (2^-S with S > 126).
+__device__ __forceinline__ float sp_phi2_prod(float u) {
+  return lg2_ftz((1.0f + u) * rcp_ftz(fmaxf(1.0f - u, 1e-12f)));
 }
 
 template <class G, int Z, int E>
@@ -191,9 +193,9 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
           if constexpr (r < Geo::RB) {
             if (!geo.template live<r>()) return;
             constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            float ph[d], rt[d];
+            float rt[d];
             uint32_t sg = 0, hs = 0;
-            float ssum = 0.0f;
+            float rtot = 1.0f;
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
@@ -202,16 +204,16 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               float x = __half2float(th);
               if constexpr (!(D1 && sp_col_deg1<G, e>())) x -= __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
-              ph[p] = sp_phi2(fabsf(x) * kLog2e, rt[p]);
-              ssum += ph[p];
+              rt[p] = sp_ratio(fabsf(x) * kLog2e);
+              rtot *= rt[p];
             });
             const uint32_t par = __popc(sg) & 1u;
-            const float e2s = ex2_ftz(-ssum);
+            const float inv = rcp_ftz(rtot);  // 2^-S; 0 once the product overflows
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
               if constexpr (D1 && sp_col_deg1<G, e>()) return;
-              const float m = fminf(sp_phi2_excl(ssum - ph[p], e2s, rt[p]) * kLn2, 30.0f);
+              const float m = fminf(sp_phi2_prod(inv * rt[p]) * kLn2, 30.0f);
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
