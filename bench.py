@@ -388,7 +388,7 @@ def sum_product_rate(a, pipe, rank, world, dist, steps=2):
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
             "decoder_ms_per_launch": sum(d0.elapsed_time(d1) for d0, d1 in dec) / steps,
             "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
-            "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi)"}
+            "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi, product-domain check update)"}
 
 
 def _wall_max(dist, secs):
