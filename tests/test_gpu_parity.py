@@ -505,6 +505,30 @@ def test_sum_product_runtime_geometry_decoder(k, n, m, ebno):
     assert np.array_equal(lb.ldpc5g_decode(llr, code, 20, "sum-product", mode="fast"), hard)
 
 
+@pytest.mark.parametrize("k,n", [(256, 512), (8448, 16896), (4096, 12288)])
+def test_sum_product_erasures_and_saturated_checks(k, n):
+    """Product-domain check update at its edges: erased (0) LLRs give ratios
+    near 2^41 whose per-check product overflows fp32, saturated LLRs give
+    1 - u below fp32 resolution.  Messages stay finite and the hard decisions
+    match the reference's sum-product (ldpc.py:139-143)."""
+    rng = np.random.default_rng(5)
+    code = lb.LdpcCode5G(k, n)
+    bits = rng.integers(0, 2, (6, k), dtype=np.uint8)
+    tx = lb.ldpc5g_encode(bits, code)
+    llr = ((2.0 * tx - 1.0) * 30.0).astype(np.float32)  # saturated, consistent with the codeword
+    llr[1:4][rng.random((3, n)) < 0.3] = 0.0              # 30 % erasures
+    llr[4] = 0.0                                           # total erasure
+    llr[5, : n // 2] *= 1e-3                               # half of the block nearly erased
+    res = lb.qc_decode(llr, code, 20, "sum-product", early_stop=False, want_llr=True)
+    assert torch.isfinite(res["llr"]).all()
+    hard = res["hard"].cpu().numpy()
+    ref_hard, _, _ = O.decode(llr, O.code(k, n), 20, "sum-product", 0.75, False)
+    ok_ref = (ref_hard == bits).all(axis=1)
+    assert ok_ref[[0, 2, 3, 5]].all()
+    assert np.array_equal(hard[ok_ref], ref_hard[ok_ref])
+    assert not hard[4].any() and not ref_hard[4].any()  # no information: ties decide 0
+
+
 def test_sum_product_runtime_geometry_equals_specialised_instance():
     k, n = 8448, 16896
     bits, llr = _oracle_llrs(k, n, 4, 4.6, 6, 4)
