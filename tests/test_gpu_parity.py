@@ -519,7 +519,7 @@ def test_sum_product_erasures_and_saturated_checks(k, n):
     llr[1:4][rng.random((3, n)) < 0.3] = 0.0              # 30 % erasures
     llr[4] = 0.0                                           # total erasure
     llr[5, : n // 2] *= 1e-3                               # half of the block nearly erased
-    res = lb.qc_decode(llr, code, 20, "sum-product", early_stop=False, want_llr=True)
+    res = lb.qc_decode(llr, code, 20, "sum-product", early_stop=False, want_llr=True, prune=True)
     assert torch.isfinite(res["llr"]).all()
     hard = res["hard"].cpu().numpy()
     ref_hard, _, _ = O.decode(llr, O.code(k, n), 20, "sum-product", 0.75, False)
