@@ -13,6 +13,9 @@
 //            R = prod 2^phi = 2^S, 2^-(S - phi_e) = 2^phi_e / R,
 //            c2v_new = sign * clip(phi(max(S - phi_e, 1e-12)), 0, 30) (rcp/lg2 MUFU)
 //   VN phase (thread = lane j, column slot): gather + clip +-40
+// Messages and posteriors are held in base-2 units (LLR * log2(e)): the phi
+// arguments and results need no rescaling per edge; the channel value is
+// scaled once per column and the mother LLR output once per variable.
 // Shared memory: E_live*Z halves of messages + NCOL*Z halves of posteriors
 // (207 KB for BG1, Z=384, 24 live rows).  Channel LLRs are re-read from the
 // rate-matched input (L2-resident) in each VN phase.
@@ -36,11 +39,10 @@ struct QcShapeSP {
 
 // phi(x) = -log(tanh(x/2)) on the reference's clip range [1e-12, 40], in
 // base-2 units: phi2(y) = phi(y ln2) / ln2 for y = x log2(e), so that
-// 2^-y = e^-x; only the outgoing message is converted back to natural LLR
-// units.  2^phi2 = (1 + u) / (1 - u) with u = 2^-y; 1 - u comes from its
+// 2^-y = e^-x.  2^phi2 = (1 + u) / (1 - u) with u = 2^-y; 1 - u comes from its
 // Taylor series for small y (no cancellation).  Flush-to-zero MUFU forms (ex2,
 // rcp, lg2, no denormal fix-ups): every operand here is a normal float.
-constexpr float kPhiLo2 = 1e-12f * kLog2e, kPhiHi2 = 40.0f * kLog2e;
+constexpr float kPhiLo2 = 1e-12f * kLog2e, kClip2 = 40.0f * kLog2e;
 
 // 1 - 2^-y without cancellation: its Taylor series for small y
 __device__ __forceinline__ float sp_one_minus(float y, float u) {
@@ -52,9 +54,11 @@ __device__ __forceinline__ float sp_one_minus(float y, float u) {
 // Product-domain check update (k_qc_sp): the check keeps the running product
 // R = prod_e ratio_e = 2^S instead of the sum S of the per-edge phi, so the
 // first phi needs no lg2 and the check no ex2 (4 MUFU per edge instead of 5).
-// ratio of the clipped argument y: 2^phi2(y) = (1 + u) / (1 - u), u = 2^-y
+// ratio of the clipped argument y: 2^phi2(y) = (1 + u) / (1 - u), u = 2^-y.
+// The reference's upper clip (40) is not applied: above it u < 2^-57 and the
+// ratio rounds to 1 either way.
 __device__ __forceinline__ float sp_ratio(float y) {
-  y = fminf(fmaxf(y, kPhiLo2), kPhiHi2);
+  y = fmaxf(y, kPhiLo2);
   const float u = ex2_ftz(-y);
   return (1.0f + u) * rcp_ftz(sp_one_minus(y, u));
 }
@@ -64,7 +68,9 @@ __device__ __forceinline__ float sp_ratio(float y) {
 // whose other edges are all very reliable (1 - u below fp32 resolution) the
 // message saturates near phi(1e-12) = 28.3 instead of its exact >= 17 value.
 // A product past the fp32 range gives u = 0 and a zero message, the fp16
-// value of the exact one (2^-S with S > 126).
+// value of the exact one (2^-S with S > 126).  The floor bounds the result
+// by log2(2e12) = 40.9 (28.3 in natural units), so the reference's message
+// clip at 30 (ldpc.py:143) never binds and is not applied.
 __device__ __forceinline__ float sp_phi2_prod(float u) {
   return lg2_ftz((1.0f + u) * rcp_ftz(fmaxf(1.0f - u, 1e-12f)));
 }
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
   const int64_t b = blockIdx.x;
   const float *row = llr + b * (int64_t)P.n;
 
-  for (int v = t; v < NCOLZ; v += NT) tot[v] = __float2half_rn(chan_value(P, row, v));
+  for (int v = t; v < NCOLZ; v += NT) tot[v] = __float2half_rn(chan_value(P, row, v) * kLog2e);
   for (int q = t; q < geo.ne() * Z; q += NT) c2v[q] = __float2half_rn(0.0f);
   __syncthreads();
 
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               float x = __half2float(th);
               if constexpr (!(D1 && sp_col_deg1<G, e>())) x -= __half2float(c2v[geo.template ez<e>() + il]);
               sg |= (__float_as_uint(x) >> 31) << p;
-              rt[p] = sp_ratio(fabsf(x) * kLog2e);
+              rt[p] = sp_ratio(fabsf(x));
               rtot *= rt[p];
             });
             const uint32_t par = __popc(sg) & 1u;
@@ -213,7 +219,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               constexpr int e = decltype(ec)::value;
               constexpr int p = e - e0;
               if constexpr (D1 && sp_col_deg1<G, e>()) return;
-              const float m = fminf(sp_phi2_prod(inv * rt[p]) * kLn2, 30.0f);
+              const float m = sp_phi2_prod(inv * rt[p]);
               const bool neg = (par ^ (sg >> p)) & 1u;
               c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
             });
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
           if constexpr (c < Geo::NCOL_MAX) {
             if constexpr (D1 && sp_col_is_deg1<G, c>()) return;
             if (c >= geo.ncol()) return;
-            float sum = chan_value(P, row, c * Z + j);
+            float sum = chan_value(P, row, c * Z + j) * kLog2e;
             constexpr int q0 = G::col_start[c], q1 = G::col_start[c + 1];
             sfor<q0, q1>([&](auto qc) {
               constexpr int e = G::col_entry[decltype(qc)::value];
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
                 if (geo.template live<G::row[e]>()) sum += __half2float(c2v[geo.template src<e>(j)]);
               }
             });
-            tot[c * Z + j] = __float2half_rn(fminf(fmaxf(sum, -40.0f), 40.0f));
+            tot[c * Z + j] = __float2half_rn(fminf(fmaxf(sum, -kClip2), kClip2));
           }
         });
       });
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
   if (iters_used && t == 0) iters_used[b] = used;
   if (llr_out) {
     float *o = llr_out + b * (int64_t)P.n_full;
-    for (int v = t; v < P.n_full; v += NT) o[v] = v < NCOLZ ? -__half2float(tot[v]) : -chan_value(P, row, v);
+    for (int v = t; v < P.n_full; v += NT) o[v] = v < NCOLZ ? -__half2float(tot[v]) * kLn2 : -chan_value(P, row, v);
   }
   unsigned err = 0;
   for (int v = t; v < P.k; v += NT) {
