@@ -44,11 +44,13 @@ struct QcShapeSP {
 // rcp, lg2, no denormal fix-ups): every operand here is a normal float.
 constexpr float kPhiLo2 = 1e-12f * kLog2e, kClip2 = 40.0f * kLog2e;
 
-// 1 - 2^-y without cancellation: its Taylor series for small y
+// 1 - 2^-y without cancellation: its Taylor series for small y.  Two terms
+// below y = 0.01 (truncation 8e-6 relative; 1 - u there carries the MUFU ex2
+// error, ~2e-5 relative at the switch), both far below the fp16 message step.
 __device__ __forceinline__ float sp_one_minus(float y, float u) {
-  // 1 - 2^-y = y ln2 - (y ln2)^2 / 2 + (y ln2)^3 / 6 - ...
-  const float series = y * fmaf(y, fmaf(y, kLn2 * kLn2 * kLn2 / 6.0f, -kLn2 * kLn2 / 2.0f), kLn2);
-  return y < 0.09f ? series : 1.0f - u;
+  // 1 - 2^-y = y ln2 - (y ln2)^2 / 2 + ...
+  const float series = y * fmaf(y, -kLn2 * kLn2 / 2.0f, kLn2);
+  return y < 0.01f ? series : 1.0f - u;
 }
 
 // Product-domain check update (k_qc_sp): the check keeps the running product
@@ -220,8 +222,8 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               constexpr int p = e - e0;
               if constexpr (D1 && sp_col_deg1<G, e>()) return;
               const float m = sp_phi2_prod(inv * rt[p]);
-              const bool neg = (par ^ (sg >> p)) & 1u;
-              c2v[geo.template ez<e>() + il] = __float2half_rn(neg ? -m : m);
+              const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
+              c2v[geo.template ez<e>() + il] = __float2half_rn(__uint_as_float(__float_as_uint(m) ^ neg));
             });
             if constexpr (ES) synx |= hs;
           }
