@@ -172,6 +172,14 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
 #define LS_QC_GENERIC 2
 #define LS_QC_FP16 4 /* packed fp16x2 kernel: two codewords per 32-bit lane */
 #define LS_QC_SP 8   /* ls_qc_has_kernel only: ask for the sum-product kernel */
+/* LS_QC_EXACT: the on-chip EXACT decoder (min-sum / scaled-min-sum only):
+ * bit-identical llr_out, hard decisions and iteration counts to the
+ * reference bp_decode on the whole mother graph (ldpc.py:86-172; never
+ * pruned), f64 messages held as a compressed per-check state in shared
+ * memory + L2.  With LS_QC_MOTHER the input is mother LLRs [B,n_full]
+ * (bp_decode on code.pcm, no derate) and hard_k receives [B,n_full]. */
+#define LS_QC_EXACT 16
+#define LS_QC_MOTHER 32
 int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
                  double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,
                  int32_t *iters_used, const uint8_t *ref_bits, unsigned long long *counts,

@@ -27,6 +27,8 @@ GEN = os.path.join(ROOT, "build", "gen")
 # per-source extra flags: the numpy-replica RNG must round every operation
 # separately, as the host libm/numpy code it mirrors does
 EXTRA = {"rng_normal.cu": ["-fmad=false"]}
+# the exact decoders reproduce numpy's separately rounded f64 operations
+EXTRA_PREFIX = {"qcx_": ["-fmad=false"]}
 
 
 def _instance_sources():
@@ -65,6 +67,15 @@ def _instance_sources():
                 f"  return launch_qc_sprt<BG{bg}Tables, {rb}, {sp}>(P, R, s, col, l, B, it, a, es, h, lo, iu, ref, cnt, st);\n"
                 "}\n}  // namespace lsb\n")
         out.append(_write(f"qcsprt_{bg}_{rb}_{sp}.cu", body))
+    for bg, z, ntl in re.findall(r"V\((\d+),\s*(\d+),\s*(\d+)\)", text):
+        body = (f'#include "{CSRC}/bp_qc_exact.cuh"\n'
+                "namespace lsb {\n"
+                f"int qcx_{bg}_{z}(const QcChanParams &P, const float *l, int64_t B, int it, double a, int es, int mo,\n"
+                "    uint8_t *h, int hl, float *lo, int32_t *iu, const uint8_t *ref, unsigned long long *cnt,\n"
+                "    cudaStream_t s) {\n"
+                f"  return launch_qc_exact<BG{bg}Tables, {z}, {ntl}>(P, l, B, it, a, es, mo, h, hl, lo, iu, ref, cnt, s);\n"
+                "}\n}  // namespace lsb\n")
+        out.append(_write(f"qcx_{bg}_{z}.cu", body))
     return out
 
 
@@ -83,7 +94,8 @@ def _compile(src: str, verbose: bool, newest_hdr: float, force: bool) -> str:
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_hdr)):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []),
+           *[f for p, fl in EXTRA_PREFIX.items() if os.path.basename(src).startswith(p) for f in fl], "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1099,12 +1099,16 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
                                                reinterpret_cast<const char *>(chn));
     const int bad0 = __syncthreads_or(lane && ((synx >> 15) & 1u));
     const int bad1 = __syncthreads_or(lane && (synx >> 31));
-    bool freed = false;
+    // both_free is decided from block-uniform values only: re-reading
+    // slot_cw after the barrier would race with thread 0's refill at the
+    // top of the next pass
+    bool freed = false, busy = false;
     for (int q = 0; q < 2; ++q) {
       const long long cw = q ? cw1 : cw0;
       if (cw < 0) continue;
       const int itq = slot_it[q];
       const bool conv = itq > 0 && !(q ? bad1 : bad0);
+      busy |= !(conv || itq == num_iter);
       if (conv || itq == num_iter) {
         if (vec & 2)
           h2_emit_vec1(P, tot, cw, q, itq, hard_k, iters_used, ref, counts, red, t, NT);
@@ -1118,7 +1122,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, 1)
     }
     if (freed) {
       __syncthreads();
-      if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
+      if (!busy) continue;  // both free: refill before iterating
     }
     h2_vn<Geo, D1>(st, tot, chn, base, h, lane, t, chan_word, geo);
     if (t == 0) {
@@ -1252,12 +1256,16 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
                                                  reinterpret_cast<const char *>(C));
     const int bad0 = __syncthreads_or((synx >> 15) & 1u);
     const int bad1 = __syncthreads_or(synx >> 31);
-    bool freed = false;
+    // both_free is decided from block-uniform values only: re-reading
+    // slot_cw after the barrier would race with thread 0's refill at the
+    // top of the next pass
+    bool freed = false, busy = false;
     for (int q = 0; q < 2; ++q) {
       const long long cw = q ? cw1 : cw0;
       if (cw < 0) continue;
       const int itq = slot_it[q];
       const bool conv = itq > 0 && !(q ? bad1 : bad0);
+      busy |= !(conv || itq == num_iter);
       if (conv || itq == num_iter) {
         if (vec & 2) {
           h2_emit_vec1(P, smw, cw, q, itq, hard_k, iters_used, ref, counts, red, t, NT, 2 * Z);
@@ -1281,7 +1289,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     }
     if (freed) {
       __syncthreads();
-      if (slot_cw[0] < 0 && slot_cw[1] < 0) continue;  // both free: refill before iterating
+      if (!busy) continue;  // both free: refill before iterating
     }
     h2w_vn<Geo>(st, smw, h, t);
     if (t == 0) {

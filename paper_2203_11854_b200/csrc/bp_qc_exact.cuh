@@ -1,0 +1,368 @@
+// EXACT-mode QC flooding BP decoder, on chip (ldpc.py:86-172 for min-sum and
+// scaled-min-sum; ldpc5g_decode ldpc.py:354-365 with derate_match 335-345
+// fused in).  Bit-identical to the reference: same f32 posterior rounding,
+// f64 messages, numpy add.reduceat summation order, tie rule and per-row
+// early stop, with NO dead-row pruning.
+//
+// Why a compressed check state is exact.  In min-sum every message leaving a
+// check is sign * alpha * (min1 or min2) of that check's |v2c| values
+// (ldpc.py:144-148, _segment_min2 65-74).  Tracking the multiset minimum
+// pair (min1, second smallest with multiplicity) and the first argmin gives
+// the reference's result: with a unique minimum the runner-up is the min over
+// the other entries, and with a tie it equals min1, which is what the
+// reference sends on every edge.  So a check is (alpha*min1, alpha*min2) in
+// f64 plus one word with the argmin position and the outgoing sign bits
+// (row parity already XORed in); (-alpha)*x == -(alpha*x) exactly, so the
+// sign is a bit flip.
+//
+// Data layout for one codeword per CTA (persistent, one CTA per SM at
+// Z = 384):
+//   shared  M1 [MB][Z] f64     alpha*min1 of every check
+//           W  [MB][Z] u16/u32 argmin << deg | outgoing signs (u32 only for
+//                              rows whose deg + log2(deg) > 16)
+//           T  [KBC][Z] f32    posteriors of the core columns (systematic +
+//                              4 core parity; KBC = k_b + 4)
+//   global  m2 [MB][Z] f64     alpha*min2 per check, one slice per CTA: read
+//                              once per check in the CN phase and once per
+//                              argmin edge in the VN phase, L2-resident
+//           channel LLRs       read from the input row each iteration (L2)
+// Config 2 (BG1, Z = 384): 141,312 + 38,400 + 39,936 = 219,648 B of shared
+// memory.  The degree-1 extension columns keep no posterior: their value
+// clip(f32(chan + c2v)) is formed inside the check update of their row.
+//
+// One iteration (flooding, ldpc.py:131-153):
+//   CN phase  thread (group g, lane i) walks the rows of its group: old c2v
+//             from the compressed state, v2c = f64(total) - c2v_old, new
+//             (min1, min2, argmin, signs); the syndrome of the totals it
+//             reads is the early-stop test of the PREVIOUS iteration
+//             (ldpc.py:155-160), so a converged codeword stops before its
+//             next variable update and its posteriors are still in T.
+//   VN phase  thread (group g, lane j) walks the core columns of its group:
+//             gathers c2v of its column in ascending check order and sums
+//             x0 + pairwise(x1..) (numpy reduceat / pairwise_sum), then
+//             total = clip(f32(f64(chan) + sum), +-40).
+// Rows and core columns are split over NTL thread groups in contiguous,
+// degree-balanced ranges; the whole base graph is compile-time, so every
+// shift, column and position is an immediate.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "bp_fast_qc.cuh"
+#include "common.cuh"
+
+namespace lsb {
+
+template <class G_, int Z_, int NTL_>
+struct QxGeo {
+  using G = G_;
+  static constexpr int Z = Z_, NTL = NTL_;
+  static constexpr int NT1 = ((Z + 31) / 32) * 32, NT = NT1 * NTL;
+  static constexpr int MB = G::MB, NB = G::NB, KBC = G::KB + 4, NEXT = G::NB - (G::KB + 4);
+  static constexpr int MINB = NT >= 768 ? 1 : (NT >= 384 ? 2 : (NT >= 256 ? 4 : 1024 / NT));
+
+  static constexpr int deg(int r) { return G::row_start[r + 1] - G::row_start[r]; }
+  static constexpr int cdeg(int c) { return G::col_start[c + 1] - G::col_start[c]; }
+  static constexpr int argbits(int d) {
+    int b = 0;
+    while ((1 << b) < d) ++b;
+    return b;
+  }
+  static constexpr int wbytes(int r) { return deg(r) + argbits(deg(r)) <= 16 ? 2 : 4; }
+  static constexpr int woff(int r) {  // byte offset of row r's word array
+    int o = 8 * MB * Z;
+    for (int q = 0; q < r; ++q) {
+      if (wbytes(q) == 4) o = (o + 3) & ~3;
+      o += wbytes(q) * Z;
+    }
+    if (wbytes(r) == 4) o = (o + 3) & ~3;
+    return o;
+  }
+  static constexpr int T_OFF = (woff(MB - 1) + wbytes(MB - 1) * Z + 15) & ~15;
+  static constexpr int SMEM = T_OFF + 4 * KBC * Z;
+
+  // contiguous degree-balanced ranges: rows [rfirst(g), rfirst(g+1)) and
+  // core columns [cfirst(g), cfirst(g+1)) belong to thread group g
+  static constexpr int rfirst(int g) {
+    if (g <= 0) return 0;
+    if (g >= NTL) return MB;
+    const int tot = G::row_start[MB];
+    int r = 0;
+    while (r < MB && G::row_start[r] * NTL < tot * g) ++r;
+    return r;
+  }
+  static constexpr int cfirst(int g) {
+    if (g <= 0) return 0;
+    if (g >= NTL) return KBC;
+    const int tot = G::col_start[KBC];
+    int c = 0;
+    while (c < KBC && G::col_start[c] * NTL < tot * g) ++c;
+    return c;
+  }
+  // thread group owning row r / core column c (compile-time only: the
+  // tables are host constexpr arrays)
+  static constexpr int rowner(int r) {
+    int g = 0;
+    while (g + 1 < NTL && r >= rfirst(g + 1)) ++g;
+    return g;
+  }
+  static constexpr int cowner(int c) {
+    int g = 0;
+    while (g + 1 < NTL && c >= cfirst(g + 1)) ++g;
+    return g;
+  }
+};
+
+// x with its sign bit flipped when `bit` is 1 (c2v = (-alpha)*excl)
+__device__ __forceinline__ double qx_flip(double x, uint32_t bit31) {
+  return __hiloint2double(__double2hiint(x) ^ (int)bit31, __double2loint(x));
+}
+
+// numpy pairwise_sum of N compile-time terms (loops_utils.h.src): fewer
+// than 8 terms sequentially from -0.0, else 8 strided accumulators, their
+// tree, then the remainder in order
+template <int N>
+__device__ __forceinline__ double qx_pairwise(const double *x) {
+  if constexpr (N < 8) {
+    double r = -0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) r = __dadd_rn(r, x[q]);
+    return r;
+  } else {
+    double r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = x[q];
+    constexpr int NB8 = N - N % 8;
+#pragma unroll
+    for (int q = 8; q < NB8; q += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = __dadd_rn(r[u], x[q + u]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int q = NB8; q < N; ++q) res = __dadd_rn(res, x[q]);
+    return res;
+  }
+}
+
+__device__ __forceinline__ float qx_clip(float x) { return fminf(fmaxf(x, -40.0f), 40.0f); }
+
+// channel value -llr of mother VN v: fused derate_match (rate-matched input)
+// or the mother LLRs themselves (bp_decode on the code's pcm)
+__device__ __forceinline__ float qx_chan(const QcChanParams &P, const float *__restrict__ row, int v, bool mother) {
+  return mother ? -__ldg(row + v) : chan_value(P, row, v);
+}
+
+template <class Geo, bool ES, bool OUT>
+__global__ void __launch_bounds__(Geo::NT, Geo::MINB)
+    k_qc_exact(const QcChanParams P, const float *__restrict__ llr, int64_t batch, int num_iter, double alpha,
+               int mother, uint8_t *__restrict__ hard, int hard_len, float *__restrict__ llr_out,
+               int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
+               unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next,
+               double *__restrict__ m2ws, float *__restrict__ extws) {
+  using G = typename Geo::G;
+  constexpr int Z = Geo::Z, NT1 = Geo::NT1, NT = Geo::NT, MB = Geo::MB, KBC = Geo::KBC;
+  extern __shared__ __align__(16) unsigned char qx_sm[];
+  double *M1 = reinterpret_cast<double *>(qx_sm);
+  float *T = reinterpret_cast<float *>(qx_sm + Geo::T_OFF);
+  __shared__ long long cur;
+  __shared__ unsigned red[NT / 32];
+  const int t = threadIdx.x, grp = t / NT1, ln = t - grp * NT1;
+  const bool lane = ln < Z;
+  double *m2 = m2ws + (size_t)blockIdx.x * MB * Z;
+  float *ext = OUT ? extws + (size_t)blockIdx.x * Geo::NEXT * Z : nullptr;
+  const bool moth = mother != 0;
+  const int row_len = moth ? P.n_full : P.n;
+
+  for (;;) {
+    if (t == 0) {
+      const unsigned long long c = atomicAdd(next, 1ULL);
+      cur = (long long)c < batch ? (long long)c : -1;
+    }
+    __syncthreads();
+    const long long cw = cur;
+    if (cw < 0) return;
+    const float *row = llr + cw * (int64_t)row_len;
+    for (int v = t; v < KBC * Z; v += NT) T[v] = qx_chan(P, row, v, moth);
+    __syncthreads();
+
+    int used = num_iter;
+    for (int it = 0; it < num_iter; ++it) {
+      const bool first = it == 0;
+      uint32_t bad = 0;
+      // ------------------------------------------------ check-node phase
+      if (lane) {
+        const int i = ln;
+        sfor<0, MB>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          if (grp != Geo::rowner(r)) return;  // warp-uniform
+          constexpr int e0 = G::row_start[r], D = Geo::deg(r);
+          using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+          WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
+          const double m1o = first ? 0.0 : M1[r * Z + i];
+          const double m2o = first ? 0.0 : m2[r * Z + i];
+          const uint32_t wo = first ? 0u : (uint32_t)W[i];
+          const uint32_t argo = wo >> D;
+          double mn1 = INFINITY, mn2 = INFINITY;
+          uint32_t arg = 0, sg = 0, syn = 0;
+          sfor<0, D>([&](auto pc) {
+            constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
+            const double cold = qx_flip(argo == (uint32_t)p ? m2o : m1o, (wo << (31 - p)) & 0x80000000u);
+            int j = i + s;
+            j = j >= Z ? j - Z : j;
+            float tv;
+            if constexpr (c < KBC) {
+              tv = T[c * Z + j];
+            } else {
+              // degree-1 extension VN: its posterior is chan + its only message
+              const float ch = qx_chan(P, row, c * Z + j, moth);
+              tv = first ? ch : qx_clip(__double2float_rn(__dadd_rn((double)ch, cold)));
+              if (OUT && ES) ext[(c - KBC) * Z + j] = tv;
+            }
+            if (ES) syn ^= __float_as_uint(tv);
+            const double x = __dsub_rn((double)tv, cold);
+            const double a = fabs(x);
+            arg = a < mn1 ? (uint32_t)p : arg;
+            mn2 = fmin(mn2, fmax(mn1, a));
+            mn1 = fmin(mn1, a);
+            sg |= ((uint32_t)__double2hiint(x) >> 31) << p;
+          });
+          bad |= syn >> 31;
+          const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
+          M1[r * Z + i] = __dmul_rn(alpha, mn1);
+          m2[r * Z + i] = __dmul_rn(alpha, mn2);
+          W[i] = (WT)(osg | (arg << D));
+        });
+      }
+      if (ES && !first) {
+        // syndrome of the posteriors of iteration `it` (ldpc.py:155-160)
+        if (!__syncthreads_or(bad)) {
+          used = it;
+          break;
+        }
+      } else {
+        __syncthreads();
+      }
+      // ------------------------------------------------ variable-node phase
+      if (lane) {
+        const int j = ln;
+        sfor<0, KBC>([&](auto cc) {
+          constexpr int c = decltype(cc)::value;
+          if (grp != Geo::cowner(c)) return;  // warp-uniform
+          constexpr int d = Geo::cdeg(c), cs = G::col_start[c];
+          const float ch = qx_chan(P, row, c * Z + j, moth);
+          double x[d];
+          sfor<0, d>([&](auto tc) {
+            constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
+            constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
+            using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+            const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
+            int i = j - s;
+            i = i < 0 ? i + Z : i;
+            const uint32_t w = W[i];
+            const double mag = (w >> D) == (uint32_t)p ? m2[r * Z + i] : M1[r * Z + i];
+            x[q] = qx_flip(mag, (w << (31 - p)) & 0x80000000u);
+          });
+          double sum = x[0];
+          if constexpr (d > 1) sum = __dadd_rn(x[0], qx_pairwise<d - 1>(x + 1));
+          T[c * Z + j] = qx_clip(__double2float_rn(__dadd_rn((double)ch, sum)));
+        });
+      }
+      __syncthreads();
+    }
+
+    // ------------------------------------------------ outputs
+    if (OUT && used == num_iter) {
+      // extension posteriors after the last variable update: chan + c2v
+      if (lane) {
+        const int i = ln;
+        sfor<4, MB>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          if (grp != Geo::rowner(r)) return;
+          constexpr int D = Geo::deg(r), e = G::row_start[r + 1] - 1, c = G::col[e], s = G::shift[e] % Z;
+          if constexpr (c >= KBC) {
+            using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+            const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
+            const uint32_t w = W[i];
+            const double mag = (w >> D) == (uint32_t)(D - 1) ? m2[r * Z + i] : M1[r * Z + i];
+            const double cv = qx_flip(mag, (w << (31 - (D - 1))) & 0x80000000u);
+            int j = i + s;
+            j = j >= Z ? j - Z : j;
+            const float ch = qx_chan(P, row, c * Z + j, moth);
+            ext[(c - KBC) * Z + j] = qx_clip(__double2float_rn(__dadd_rn((double)ch, cv)));
+          }
+        });
+      }
+      __syncthreads();
+    }
+    if (iters_used && t == 0) iters_used[cw] = used;
+    if (OUT && llr_out) {
+      float *o = llr_out + cw * (int64_t)P.n_full;
+      for (int v = t; v < P.n_full; v += NT) o[v] = -(v < KBC * Z ? T[v] : ext[v - KBC * Z]);
+    }
+    unsigned err = 0;
+    if (hard || ref) {
+      for (int v = t; v < hard_len; v += NT) {
+        const float tv = v < KBC * Z ? T[v] : (OUT ? ext[v - KBC * Z] : 0.0f);
+        const uint8_t h = (-tv) > 0.0f;
+        if (hard) hard[cw * (int64_t)hard_len + v] = h;
+        if (ref && v < P.k) err += (h != ref[cw * (int64_t)P.k + v]);
+      }
+    }
+    if (ref && counts) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+      if ((t & 31) == 0) red[t >> 5] = err;
+      __syncthreads();
+      if (t == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < NT / 32; ++w) s += red[w];
+        if (s) {
+          atomicAdd(&counts[0], s);
+          atomicAdd(&counts[1], 1ULL);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// one exact-decoder instance: persistent grid, one L2 slice of min2 per CTA
+template <class G, int Z, int NTL>
+int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_iter, double alpha, int early_stop,
+                    int mother, uint8_t *hard, int hard_len, float *llr_out, int32_t *iters_used, const uint8_t *ref,
+                    unsigned long long *counts, cudaStream_t s) {
+  using Geo = QxGeo<G, Z, NTL>;
+  static_assert(Geo::SMEM <= 227 * 1024, "exact decoder state does not fit in shared memory");
+  const bool out = llr_out != nullptr || hard_len > Geo::KBC * Z;
+  auto kern = early_stop ? (out ? k_qc_exact<Geo, true, true> : k_qc_exact<Geo, true, false>)
+                         : (out ? k_qc_exact<Geo, false, true> : k_qc_exact<Geo, false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(exact smem attr)");
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Geo::NT, Geo::SMEM);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), B);
+  if (grid <= 0) return LS_OK;
+  const size_t m2_bytes = sizeof(double) * (size_t)grid * Geo::MB * Z;
+  const size_t ext_bytes = out ? sizeof(float) * (size_t)grid * Geo::NEXT * Z : 0;
+  char *ws = nullptr;
+  retain_pool_memory();
+  e = cudaMallocAsync((void **)&ws, 256 + m2_bytes + ext_bytes, s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(exact workspace)");
+  unsigned long long *next = reinterpret_cast<unsigned long long *>(ws);
+  cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+  double *m2 = reinterpret_cast<double *>(ws + 256);
+  float *ext = out ? reinterpret_cast<float *>(ws + 256 + m2_bytes) : nullptr;
+  kern<<<(unsigned)grid, Geo::NT, Geo::SMEM, s>>>(P, llr, B, num_iter, alpha, mother, hard, hard_len, llr_out,
+                                                   iters_used, ref, counts, next, m2, ext);
+  e = cudaGetLastError();
+  cudaFreeAsync(ws, s);
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode(exact)");
+}
+
+}  // namespace lsb

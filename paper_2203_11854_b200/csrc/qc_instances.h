@@ -64,3 +64,13 @@
   W(1, 46, 2)                    \
   W(2, 22, 2)                    \
   W(2, 42, 2)
+
+// On-chip EXACT-mode decoders (bp_qc_exact.cuh): base graph, Z, thread
+// groups per lane.  Bit-identical min-sum / scaled-min-sum on the whole
+// mother graph; codes without an instance use the HBM-streaming CSR decoder
+// (bp_exact.cu).
+//   1,384 : config 2        1,192 : configs 3 and 4       2,26 : config 1
+#define LSB_QCX_INSTANCES(V) \
+  V(1, 384, 2)               \
+  V(1, 192, 2)               \
+  V(2, 26, 2)

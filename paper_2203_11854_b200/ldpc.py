@@ -14,6 +14,7 @@
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -115,6 +116,8 @@ class LdpcCode5G:
             ptr = np.zeros(self.m_full + 1, np.int64)
             ptr[1:] = np.cumsum(np.bincount(rows, minlength=self.m_full))
             self._pcm = ParityCheckMatrix._trusted(self.n_full, self.m_full, ptr, cols)
+            # lets bp_decode(llr, code.pcm) take the on-chip QC exact decoder
+            self._pcm._qc_code = weakref.ref(self)
         return self._pcm
 
     # ------------------------------------------------------------ encoder
@@ -165,13 +168,29 @@ def _check_variant(variant: str, num_iter: int):
         raise ValueError("num_iter must be >= 1")
 
 
+def _qc_exact_code(pcm, variant: str, dtype):
+    """The LdpcCode5G behind `pcm` when the on-chip exact QC decoder serves
+    this call (min-sum / scaled-min-sum on f32 LLRs), else None."""
+    ref = getattr(pcm, "_qc_code", None)
+    code = ref() if ref is not None else None
+    if code is None or variant == "sum-product" or dtype != L.torch().float32:
+        return None
+    return code if qc_has_kernel(code, precision="exact") else None
+
+
 def bp_decode(llr, pcm: ParityCheckMatrix, num_iter: int = 20, variant: str = "sum-product",
               scale: float = 0.75, early_stop: bool = True, *, return_iters: bool = False,
-              device: bool = False):
+              device: bool = False, engine: str = "auto"):
     """Flooding BP (ldpc.py:86-172), exact mode, on the GPU.
 
     Returns (llr_out, hard) [batch, n] like the reference; with
     return_iters=True also the per-row iteration counts.
+
+    engine: "qc" is the on-chip decoder of a lifted 5G code's pcm
+    (bp_qc_exact.cuh; min-sum / scaled-min-sum on f32 LLRs), "csr" the
+    HBM-streaming decoder for any ParityCheckMatrix (bp_exact.cu); "auto"
+    takes "qc" when it serves the call.  Both are bit-identical to the
+    reference.
     """
     _check_variant(variant, num_iter)
     was_np = not L.is_tensor(llr)
@@ -184,6 +203,19 @@ def bp_decode(llr, pcm: ParityCheckMatrix, num_iter: int = 20, variant: str = "s
     if t.shape[-1] != pcm.n:
         raise ValueError(f"LLR length {t.shape[-1]} does not match n={pcm.n}")
     B = t.shape[0]
+    if engine not in ("auto", "qc", "csr"):
+        raise ValueError(f"unknown bp_decode engine {engine!r}")
+    code = _qc_exact_code(pcm, variant, t.dtype) if engine != "csr" else None
+    if engine == "qc" and code is None:
+        raise ValueError("bp_decode: the on-chip QC exact decoder does not serve this call")
+    if code is not None:
+        r = qc_decode(t, code, num_iter, variant, scale, early_stop=early_stop, want_llr=True,
+                      want_iters=True, precision="exact", mother=True)
+        out, hard, iters = r["llr"], r["hard"], r["iters"]
+        if was_np and not device:
+            res = (L.to_host(out), L.to_host(hard))
+            return res + (L.to_host(iters),) if return_iters else res
+        return (out, hard, iters) if return_iters else (out, hard)
     is64 = t.dtype == torch.float64
     out = L.empty((B, pcm.n), "float64" if is64 else "float32")
     hard = L.empty((B, pcm.n), "uint8")
@@ -202,6 +234,15 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
     """BP-decode rate-matched LLRs -> [batch, k] info bits (ldpc.py:354-365)."""
     _check_variant(variant, num_iter)
     if mode == "exact":
+        t = L.to_device(llr)
+        if t.dim() == 1:
+            t = t.unsqueeze(0)
+        if (t.dtype == L.torch().float32 and variant != "sum-product"
+                and qc_has_kernel(code, precision="exact")):
+            # on-chip exact decoder with derate_match fused in
+            out = qc_decode(t, code, num_iter, variant, scale, early_stop=early_stop,
+                            precision="exact")["hard"]
+            return L.to_host(out) if (not L.is_tensor(llr) and not device) else out
         mother = code.derate_match(llr, device=True)
         _, hard = bp_decode(mother, code.pcm, num_iter, variant, scale, early_stop, device=True)
         out = hard[:, : code.k].contiguous()
@@ -252,14 +293,17 @@ def _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, prec
     return out.numpy() if not L.is_tensor(llr) else out
 
 
-LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP = 1, 2, 4, 8
+LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP, LS_QC_EXACT, LS_QC_MOTHER = 1, 2, 4, 8, 16, 32
 
 
 def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
                   variant: str = "min-sum") -> bool:
     """Whether a compile-time specialised fast decoder exists for this code
     (the sum-product fast decoder exists only as such instances; min-sum codes
-    without one run the runtime-geometry fp16x2 or the runtime-Z fp32 kernel)."""
+    without one run the runtime-geometry fp16x2 or the runtime-Z fp32 kernel).
+    precision "exact" asks for the on-chip exact decoder (min-sum variants)."""
+    if precision == "exact":
+        return variant != "sum-product" and bool(L.lib().ls_qc_has_kernel(code.handle, LS_QC_EXACT))
     flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
     if variant == "sum-product":
         flags |= LS_QC_SP
@@ -269,7 +313,7 @@ def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
 def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum", scale: float = 0.75,
               *, early_stop: bool = True, ref_bits=None, want_hard: bool = True, want_llr: bool = False,
               want_iters: bool = False, counts=None, prune: bool | None = None, generic: bool = False,
-              precision: str = "fp32"):
+              precision: str = "fp32", mother: bool = False):
     """Fast-mode fused decoder: rate-matched f32 LLRs [B, n] on the device ->
     dict(hard [B,k] uint8, llr [B,n_full] f32 mother LLRs, iters [B] int32,
     counts [2] int64 (bit, block) errors vs ref_bits), each only if asked.
@@ -278,22 +322,31 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
     extension rows whose parity bit is never transmitted.  precision
     "fp16x2" selects the packed two-codewords-per-lane kernel.  generic forces
     the runtime-geometry kernel of that precision instead of a compile-time
-    specialised instance."""
-    if prune is None:
-        prune = not want_llr
-    if precision not in ("fp32", "fp16x2"):
+    specialised instance.  precision "exact" is the on-chip bit-exact decoder
+    (bp_qc_exact.cuh: whole mother graph, reference arithmetic; min-sum and
+    scaled-min-sum); with mother=True its input is mother LLRs [B, n_full]
+    and `hard` covers all n_full positions (bp_decode on code.pcm)."""
+    if precision not in ("fp32", "fp16x2", "exact"):
         raise ValueError(f"unknown decoder precision {precision!r}")
+    if mother and precision != "exact":
+        raise ValueError("mother-length input needs precision='exact'")
+    if precision == "exact":
+        prune = False
+    elif prune is None:
+        prune = not want_llr
     flags = ((LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
-             | (LS_QC_FP16 if precision == "fp16x2" else 0))
+             | (LS_QC_FP16 if precision == "fp16x2" else 0) | (LS_QC_EXACT if precision == "exact" else 0)
+             | (LS_QC_MOTHER if mother else 0))
     _check_variant(variant, num_iter)
     t = L.to_device(llr, "float32")
     if t.dim() == 1:
         t = t.unsqueeze(0)
-    if t.shape[-1] != code.n:
-        raise ValueError(f"expected {code.n} LLRs, got {t.shape[-1]}")
+    n_in = code.n_full if mother else code.n
+    if t.shape[-1] != n_in:
+        raise ValueError(f"expected {n_in} LLRs, got {t.shape[-1]}")
     B = t.shape[0]
     res = {}
-    hard = L.empty((B, code.k), "uint8") if want_hard else None
+    hard = L.empty((B, code.n_full if mother else code.k), "uint8") if want_hard else None
     lo = L.empty((B, code.n_full), "float32") if want_llr else None
     it = L.empty((B,), "int32") if want_iters else None
     ref = L.to_device(ref_bits, "uint8") if ref_bits is not None else None
