@@ -89,10 +89,23 @@ def _write(name: str, body: str) -> str:
 
 
 
+def _deps(path: str, seen=None) -> set:
+    """The file and every local header it includes, recursively."""
+    import re
+
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), re.M):
+        _deps(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return seen
+
+
 def _compile(src: str, verbose: bool, newest_hdr: float, force: bool) -> str:
     obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
-    if (not force and os.path.exists(obj)
-            and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_hdr)):
+    newest_dep = max(os.path.getmtime(f) for f in _deps(src))
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []),
            *[f for p, fl in EXTRA_PREFIX.items() if os.path.basename(src).startswith(p) for f in fl], "-c", src, "-o", obj]

@@ -18,8 +18,9 @@
 // Data layout for one codeword per CTA (persistent, one CTA per SM at
 // Z = 384):
 //   shared  M1 [MB][Z] f64     alpha*min1 of every check
-//           W  [MB][Z] u16/u32 argmin << deg | outgoing signs (u32 only for
-//                              rows whose deg + log2(deg) > 16)
+//           W  [MB][Z] u16/u32 argmin << deg | outgoing signs, position p
+//                              at bit deg-1-p (u32 only for rows whose
+//                              deg + log2(deg) > 16)
 //           T  [KBC][Z] f32    posteriors of the core columns (systematic +
 //                              4 core parity; KBC = k_b + 4)
 //   global  m2 [MB][Z] f64     alpha*min2 per check, one slice per CTA: read
@@ -195,46 +196,60 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       uint32_t bad = 0;
       // ------------------------------------------------ check-node phase
       if (lane) {
-        const int i = ln;
+        uint32_t i4 = 4u * (uint32_t)ln;
+        // opaque per iteration: keeps the ~600 per-edge lane offsets from
+        // being hoisted out of the iteration loop (and spilled)
+        asm volatile("" : "+r"(i4));
         sfor<0, MB>([&](auto rc) {
           constexpr int r = decltype(rc)::value;
           if (grp != Geo::rowner(r)) return;  // warp-uniform
           constexpr int e0 = G::row_start[r], D = Geo::deg(r);
           using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
           WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
-          const double m1o = first ? 0.0 : M1[r * Z + i];
-          const double m2o = first ? 0.0 : m2[r * Z + i];
-          const uint32_t wo = first ? 0u : (uint32_t)W[i];
+          const int ci = r * Z + ln;
+          double m1o = 0.0, m2o = 0.0;
+          uint32_t wo = 0u;
+          if (!first) {
+            m1o = M1[ci];
+            m2o = m2[ci];
+            wo = (uint32_t)W[ln];
+          }
           const uint32_t argo = wo >> D;
           double mn1 = INFINITY, mn2 = INFINITY;
           uint32_t arg = 0, sg = 0, syn = 0;
           sfor<0, D>([&](auto pc) {
             constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
-            const double cold = qx_flip(argo == (uint32_t)p ? m2o : m1o, (wo << (31 - p)) & 0x80000000u);
-            int j = i + s;
-            j = j >= Z ? j - Z : j;
+            // old message on this edge: +-(alpha*min1 | alpha*min2), sign
+            // bit of position p at bit D-1-p of the word
+            const double mag = argo == (uint32_t)p ? m2o : m1o;
+            const double cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
+            uint32_t o = i4 + 4u * s;  // byte offset of lane (i + s) mod Z
+            o = min(o, o - 4u * Z);
             float tv;
             if constexpr (c < KBC) {
-              tv = T[c * Z + j];
+              tv = *reinterpret_cast<const float *>(reinterpret_cast<const char *>(T) + 4 * c * Z + o);
             } else {
               // degree-1 extension VN: its posterior is chan + its only message
-              const float ch = qx_chan(P, row, c * Z + j, moth);
+              const int v = c * Z + (int)(o >> 2);
+              const float ch = qx_chan(P, row, v, moth);
               tv = first ? ch : qx_clip(__double2float_rn(__dadd_rn((double)ch, cold)));
-              if (OUT && ES) ext[(c - KBC) * Z + j] = tv;
+              if (OUT && ES) ext[v - KBC * Z] = tv;
             }
             if (ES) syn ^= __float_as_uint(tv);
             const double x = __dsub_rn((double)tv, cold);
             const double a = fabs(x);
-            arg = a < mn1 ? (uint32_t)p : arg;
-            mn2 = fmin(mn2, fmax(mn1, a));
-            mn1 = fmin(mn1, a);
-            sg |= ((uint32_t)__double2hiint(x) >> 31) << p;
+            const bool lt1 = a < mn1, lt2 = a < mn2;
+            const double t2 = lt2 ? a : mn2;
+            mn2 = lt1 ? mn1 : t2;
+            mn1 = lt1 ? a : mn1;
+            arg = lt1 ? (uint32_t)p : arg;
+            sg = __funnelshift_l((uint32_t)__double2hiint(x), sg, 1);  // signbit(x) in at bit 0
           });
           bad |= syn >> 31;
           const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
-          M1[r * Z + i] = __dmul_rn(alpha, mn1);
-          m2[r * Z + i] = __dmul_rn(alpha, mn2);
-          W[i] = (WT)(osg | (arg << D));
+          M1[ci] = __dmul_rn(alpha, mn1);
+          m2[ci] = __dmul_rn(alpha, mn2);
+          W[ln] = (WT)(osg | (arg << D));
         });
       }
       if (ES && !first) {
@@ -249,6 +264,8 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       // ------------------------------------------------ variable-node phase
       if (lane) {
         const int j = ln;
+        uint32_t j8 = 8u * (uint32_t)j;
+        asm volatile("" : "+r"(j8));
         sfor<0, KBC>([&](auto cc) {
           constexpr int c = decltype(cc)::value;
           if (grp != Geo::cowner(c)) return;  // warp-uniform
@@ -259,12 +276,15 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
             constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
-            const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
-            int i = j - s;
-            i = i < 0 ? i + Z : i;
-            const uint32_t w = W[i];
-            const double mag = (w >> D) == (uint32_t)p ? m2[r * Z + i] : M1[r * Z + i];
-            x[q] = qx_flip(mag, (w << (31 - p)) & 0x80000000u);
+            uint32_t o8 = j8 - 8u * s;  // 8 * ((j - s) mod Z)
+            o8 = min(o8, o8 + 8u * Z);
+            const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
+            double mag;
+            if ((w >> D) == (uint32_t)p)
+              mag = *reinterpret_cast<const double *>(reinterpret_cast<const char *>(m2) + 8 * r * Z + o8);
+            else
+              mag = *reinterpret_cast<const double *>(qx_sm + 8 * r * Z + o8);
+            x[q] = qx_flip(mag, (w << (32 - D + p)) & 0x80000000u);
           });
           double sum = x[0];
           if constexpr (d > 1) sum = __dadd_rn(x[0], qx_pairwise<d - 1>(x + 1));
@@ -288,7 +308,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
             const uint32_t w = W[i];
             const double mag = (w >> D) == (uint32_t)(D - 1) ? m2[r * Z + i] : M1[r * Z + i];
-            const double cv = qx_flip(mag, (w << (31 - (D - 1))) & 0x80000000u);
+            const double cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
             int j = i + s;
             j = j >= Z ? j - Z : j;
             const float ch = qx_chan(P, row, c * Z + j, moth);
