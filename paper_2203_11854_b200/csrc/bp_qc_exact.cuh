@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
                int mother, uint8_t *__restrict__ hard, int hard_len, float *__restrict__ llr_out,
                int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
                unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next,
-               double *__restrict__ m2ws, float *__restrict__ extws) {
+               double *__restrict__ m2ws, float *__restrict__ extws, float *__restrict__ chws) {
   using G = typename Geo::G;
   constexpr int Z = Geo::Z, NT1 = Geo::NT1, NT = Geo::NT, MB = Geo::MB, KBC = Geo::KBC;
   extern __shared__ __align__(16) unsigned char qx_sm[];
@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
   const bool lane = ln < Z;
   double *m2 = m2ws + (size_t)blockIdx.x * MB * Z;
   float *ext = OUT ? extws + (size_t)blockIdx.x * Geo::NEXT * Z : nullptr;
+  // channel values -derate(llr) of the current codeword, formed once per
+  // codeword (fillers, punctured positions, repetitions) and re-read from L2
+  float *chn = chws + (size_t)blockIdx.x * Geo::NB * Z;
   const bool moth = mother != 0;
   const int row_len = moth ? P.n_full : P.n;
 
@@ -187,7 +190,11 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
     const long long cw = cur;
     if (cw < 0) return;
     const float *row = llr + cw * (int64_t)row_len;
-    for (int v = t; v < KBC * Z; v += NT) T[v] = qx_chan(P, row, v, moth);
+    for (int v = t; v < Geo::NB * Z; v += NT) {
+      const float ch = qx_chan(P, row, v, moth);
+      chn[v] = ch;
+      if (v < KBC * Z) T[v] = ch;
+    }
     __syncthreads();
 
     int used = num_iter;
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             } else {
               // degree-1 extension VN: its posterior is chan + its only message
               const int v = c * Z + (int)(o >> 2);
-              const float ch = qx_chan(P, row, v, moth);
+              const float ch = chn[v];
               tv = first ? ch : qx_clip(__double2float_rn(__dadd_rn((double)ch, cold)));
               if (OUT && ES) ext[v - KBC * Z] = tv;
             }
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           constexpr int c = decltype(cc)::value;
           if (grp != Geo::cowner(c)) return;  // warp-uniform
           constexpr int d = Geo::cdeg(c), cs = G::col_start[c];
-          const float ch = qx_chan(P, row, c * Z + j, moth);
+          const float ch = chn[c * Z + j];
           double x[d];
           sfor<0, d>([&](auto tc) {
             constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             const double cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
             int j = i + s;
             j = j >= Z ? j - Z : j;
-            const float ch = qx_chan(P, row, c * Z + j, moth);
+            const float ch = chn[c * Z + j];
             ext[(c - KBC) * Z + j] = qx_clip(__double2float_rn(__dadd_rn((double)ch, cv)));
           }
         });
@@ -370,16 +377,18 @@ int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_
   if (grid <= 0) return LS_OK;
   const size_t m2_bytes = sizeof(double) * (size_t)grid * Geo::MB * Z;
   const size_t ext_bytes = out ? sizeof(float) * (size_t)grid * Geo::NEXT * Z : 0;
+  const size_t ch_bytes = sizeof(float) * (size_t)grid * Geo::NB * Z;
   char *ws = nullptr;
   retain_pool_memory();
-  e = cudaMallocAsync((void **)&ws, 256 + m2_bytes + ext_bytes, s);
+  e = cudaMallocAsync((void **)&ws, 256 + m2_bytes + ext_bytes + ch_bytes, s);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(exact workspace)");
   unsigned long long *next = reinterpret_cast<unsigned long long *>(ws);
   cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
   double *m2 = reinterpret_cast<double *>(ws + 256);
   float *ext = out ? reinterpret_cast<float *>(ws + 256 + m2_bytes) : nullptr;
+  float *chn = reinterpret_cast<float *>(ws + 256 + m2_bytes + ext_bytes);
   kern<<<(unsigned)grid, Geo::NT, Geo::SMEM, s>>>(P, llr, B, num_iter, alpha, mother, hard, hard_len, llr_out,
-                                                   iters_used, ref, counts, next, m2, ext);
+                                                   iters_used, ref, counts, next, m2, ext, chn);
   e = cudaGetLastError();
   cudaFreeAsync(ws, s);
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode(exact)");
