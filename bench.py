@@ -29,6 +29,13 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 K_INFO, N_TX, M_BITS = 8448, 16896, 4
+# kernels of one headline step (ncu launch list, profiles/r02/launches_bench.csv):
+# binary_source, encoder, mapper, 5 numpy-ziggurat kernels, demapper, exact decoder
+GPU_LAUNCHES_PER_STEP = 10
+# DRAM bytes (read + write) per codeword of k_qc_exact<BG1,384,2>, from the
+# ncu --set full capture of the bench's own decoder launch (profiles/r02/);
+# the messages never leave the SM, DRAM sees the LLR input and the counts
+EXACT_TRAFFIC_PER_CW = 94_468_608 / 1184
 METRIC = "decoded info Gbit/s (LDPC BG1, 20 iters) at 1/2/4/8 B200 vs CPU ref; %roofline"
 
 
@@ -47,7 +54,7 @@ def _args():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--no-exact", action="store_true")
+    p.add_argument("--no-extra", action="store_true")
     return p.parse_args()
 
 
@@ -111,9 +118,9 @@ def run_reference(a, rank):
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64/f32 (reference precision pattern)", "data": "synthetic",
             "config": _workload(a), "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
-                             "sample": f"{total_cw} codewords in batches of 4 per worker thread, "
-                                       f"oracle port of run_batch (numpy + C BP)"},
+            "cpu_baseline": dict({"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
+                                  "sample": f"{total_cw} codewords in batches of 4 per worker thread, "
+                                            f"oracle port of run_batch (numpy + C BP)"}, **host_info()),
             "e2e": {"value": v, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -170,6 +177,31 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ B200 arm
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def _roofline(B, bytes_cw, ms_per_launch, kernel, dec_ms, ms, traffic=None, note=None):
+    peaks = _peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = B * bytes_cw / (ms_per_launch / 1e3) / 1e9
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+         "traffic": traffic, "kernel": kernel, "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
+         "kernel_ms_per_launch": ms_per_launch, "kernel_share_of_step": dec_ms / ms,
+         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
+    if note:
+        r["note"] = note
+    return r
+
+
+def _bytes_cw(iters):
+    # VN-sweep model: I*4*N + 4*n + ceil(k/8) per codeword
+    return iters * 4 * 68 * 384 + 4 * N_TX + (K_INFO + 7) // 8
+
+
 def run_b200(a, rank, world, local_rank):
     import torch
 
@@ -190,13 +222,17 @@ def run_b200(a, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
+    # the headline chain is the reference's own arithmetic end to end: numpy-exact
+    # payload and noise streams, f64 demapper cast to f32, and the on-chip exact
+    # BP decoder (bit-identical to ldpc.py:86-172) over the whole mother graph
     cfg = lb.SimConfig.from_dict({
         "code": {"family": "ldpc5g", "k": K_INFO, "n": N_TX,
-                 "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "fast",
+                 "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "exact",
                              "early_stop": bool(a.early_stop)}},
         "modulation": {"kind": "qam", "bits_per_symbol": M_BITS},
         "sweep": {"ebno_db": [a.ebno], "batch_size": a.batch}, "seed": a.seed})
     pipe = lb.Pipeline(cfg)
+    assert pipe.qc_exact, "the on-chip exact decoder instance for config 2 is missing"
     B = a.batch
     counts = L.zeros((2,), "int64")
     stream = torch.cuda.current_stream()
@@ -212,7 +248,7 @@ def run_b200(a, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=a.early_stop, ref_bits=payload,
-                     want_hard=False, counts=counts, precision=pipe.precision)
+                     want_hard=False, counts=counts, precision="exact")
         if timed:
             e1.record(stream)
             dec_events.append((e0, e1))
@@ -241,62 +277,95 @@ def run_b200(a, rank, world, local_rank):
     ms, dec_ms = float(tm[0]), float(tm[1])
     errs = counts.cpu().tolist()
     value = world * B * K_INFO * a.steps / (ms / 1e3) / 1e9
-
-    # roofline of the dominant kernel (k_qc_fast): VN-sweep model, SURVEY.md 8d
-    n_full = 68 * 384
-    iters = a.iters
-    bytes_cw = iters * 4 * n_full + 4 * N_TX + (K_INFO + 7) // 8
-    per_launch_ms = dec_ms / a.steps
-    achieved = B * bytes_cw / (per_launch_ms / 1e3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except (OSError, ValueError):
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
     line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f16x2" if pipe.precision == "fp16x2" else "f32",
+            "vs_baseline": None, "dtype": "f32 posteriors / f64 messages (reference arithmetic, bit-exact)",
             "data": "synthetic (random payload per step)",
-            "config": dict(_workload(a), decoder_precision=pipe.precision, fused_modem=pipe.fused_modem),
-            "gpu_launches": (4 if pipe.fused_modem else 6) * a.steps,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         # DRAM bytes per launch: ncu --set full capture of k_qc_fast_h2 on 2368
-                         # codewords (184.3 MB read+write, profiles/r01/ncu_k_qc_fast_h2_v5_*), scaled to this batch;
-                         # the messages never leave the SM, DRAM sees the LLR input only
-                         "traffic": (B * 184_333_312 / 2368) if pipe.precision == "fp16x2" else None,
-                         "kernel": "k_qc_fast_h2w" if pipe.precision == "fp16x2" else "k_qc_fast2",
-                         "bytes_per_codeword": bytes_cw, "codewords_per_launch": B,
-                         "kernel_ms_per_launch": per_launch_ms,
-                         "kernel_share_of_step": dec_ms / ms,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
+            "config": dict(_workload(a), decoder="exact (on-chip, bit-identical to the reference)",
+                           noise="numpy-exact ziggurat replica", demapper="app f64 -> f32"),
+            "gpu_launches": GPU_LAUNCHES_PER_STEP * a.steps,
+            "roofline": _roofline(B, _bytes_cw(a.iters), dec_ms / a.steps, "k_qc_exact<BG1,384,2>", dec_ms, ms,
+                                  traffic=EXACT_TRAFFIC_PER_CW * B,
+                                  note="messages stay on chip (f64 min1 + argmin/sign words in shared memory, "
+                                       "min2 and channel in an L2 slice per SM); the kernel is bound by the "
+                                       "ALU issue pipe, not HBM (ncu in profiles/r02)"),
             "clocks": clk.summary(),
             "errors_in_timed_region": {"bit_errors": errs[0], "block_errors": errs[1],
                                        "blocks": world * B * a.steps}}
     if not a.no_e2e:
-        line["e2e"] = e2e_chain(a, pipe, rank, world, dist)
-        line["e2e_decode_only"] = e2e_decode(a, pipe, rank, world, dist)
-    if not a.early_stop:
-        line["early_stop_variant"] = early_stop_rate(a, pipe, rank, world, dist)
-    if a.variant != "sum-product":
-        line["sum_product_variant"] = sum_product_rate(a, pipe, rank, world, dist)
-    if not a.no_exact and rank == 0:
-        line["exact_mode"] = exact_rate(a, pipe)
+        line["e2e"] = e2e_decode(a, pipe, rank, world, dist)
+        line["e2e_run_batch"] = e2e_chain(a, pipe, rank, world, dist)
+    if not a.no_extra:
+        line["exact_early_stop"] = exact_early_stop_rate(a, pipe, rank, world, dist)
+        line["fast_fp16x2_min_sum"] = fast_rate(a, rank, world, dist, "fp16x2", prune=True)
+        line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32", prune=False)
+        line["sum_product_fast"] = sum_product_rate(a, rank, world, dist)
     if rank == 0 and world == 1 and not a.no_cpu:
         v, cw, el = cpu_chain_rate(a, a.cpu_seconds, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": v, "unit": "Gbit/s", "cores": os.cpu_count() or 1, "kind": "port",
-                                "sample": f"{cw} codewords ({el:.1f} s), oracle port of run_batch, "
-                                          f"batches of 4 per worker thread"}
+        line["cpu_baseline"] = dict({"value": v, "unit": "Gbit/s", "cores": os.cpu_count() or 1, "kind": "port",
+                                     "sample": f"{cw} codewords ({el:.1f} s), oracle port of run_batch, "
+                                               f"batches of 4 per worker thread"}, **host_info())
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def early_stop_rate(a, pipe, rank, world, dist, steps=3):
-    """Same chain with the syndrome early stop on (max 20 iterations), the
-    second BASELINE.md variant; reports the mean iterations executed."""
+def host_info():
+    """Host facts BASELINE.md section 3 asks for beside a CPU number."""
+    info = {"threads_used": os.cpu_count() or 1,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset (default)")}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+            if line.startswith("Socket(s):") or line.startswith("Core(s) per socket:"):
+                info[line.split(":")[0].strip().lower().replace(" ", "_")] = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        import numpy as np
+        import scipy
+
+        info["numpy"] = np.__version__
+        info["scipy"] = scipy.__version__
+        try:
+            cfg = np.show_config(mode="dicts")
+            blas = cfg.get("Build Dependencies", {}).get("blas", {})
+            info["blas"] = f"{blas.get('name', '?')} {blas.get('version', '')}".strip()
+        except Exception:  # pragma: no cover - numpy without the dict mode
+            pass
+    except ImportError:  # pragma: no cover
+        pass
+    info["note"] = ("oracle port (numpy + the C restatement of bp_decode), ~50x faster than the numpy "
+                    "reference itself (BASELINE.md section 4), so the GPU/CPU ratio is conservative")
+    return info
+
+
+def _timed_steps(fn, steps, dist):
+    import torch
+
+    fn(-1)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(torch.cuda.current_device()) as clk:
+        e0.record()
+        for i in range(steps):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    return float(tm[0]), clk.summary()
+
+
+def exact_early_stop_rate(a, pipe, rank, world, dist, steps=3):
+    """The exact chain with the reference's syndrome early stop (ldpc.py:155-167;
+    converged codewords leave the persistent decoder at once)."""
     import torch
 
     import paper_2203_11854_b200 as lb
@@ -306,55 +375,39 @@ def early_stop_rate(a, pipe, rank, world, dist, steps=3):
     counts = L.zeros((2,), "int64")
     iters = []
 
-    dec = []
-
     def one(i):
         payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (900 + i)))
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d0.record()
-        dec.append((d0, d1))
         r = lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=True, ref_bits=payload,
-                         want_hard=False, want_iters=True, counts=counts, precision=pipe.precision)
-        d1.record()
+                         want_hard=False, want_iters=True, counts=counts, precision="exact")
         iters.append(r["iters"])
 
-    one(-1)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters.clear()
-    dec.clear()
-    counts.zero_()
-    with Clocks(torch.cuda.current_device()) as clk:
-        e0.record()
-        for i in range(steps):
-            one(i)
-        e1.record()
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    ms = float(tm[0])
-    mean_it = float(torch.cat(iters).float().mean())
-    c = counts.cpu().tolist()
+    ms, clk = _timed_steps(one, steps, dist)
+    mean_it = float(torch.cat(iters[1:]).float().mean())
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s",
-            "mean_iterations": mean_it, "ms_per_step": ms / steps, "clocks": clk.summary(),
-            "decoder_ms_per_launch": sum(d0.elapsed_time(d1) for d0, d1 in dec) / steps,
-            "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
-            "note": "persistent fp16x2 kernel: each SM keeps two codeword slots busy and refills a slot "
-                    "as soon as its codeword's syndrome is satisfied"}
+            "mean_iterations": mean_it, "ms_per_step": ms / steps, "clocks": clk,
+            "note": "exact chain, early stop as the reference (per-codeword syndrome after each iteration)"}
 
 
-def sum_product_rate(a, pipe, rank, world, dist, steps=2):
-    """The reference's default BP variant (sum-product, ldpc.py:139-143) on the
-    same chain, fixed iterations: fp16 per-edge messages on chip, fp32 math."""
+def _fast_pipe(a, variant):
+    import paper_2203_11854_b200 as lb
+
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": K_INFO, "n": N_TX,
+                 "decoder": {"variant": variant, "num_iter": a.iters, "mode": "fast", "early_stop": False}},
+        "modulation": {"kind": "qam", "bits_per_symbol": M_BITS},
+        "sweep": {"ebno_db": [a.ebno], "batch_size": a.batch}, "seed": a.seed})
+    return lb.Pipeline(cfg)
+
+
+def fast_rate(a, rank, world, dist, precision, prune, steps=3):
+    """Statistically-equivalent fast chain (fused Philox modem + on-chip
+    decoder), labelled: not the reference arithmetic."""
     import torch
 
     import paper_2203_11854_b200 as lb
     from paper_2203_11854_b200 import _lib as L
 
+    pipe = _fast_pipe(a, a.variant)
     B = a.batch
     counts = L.zeros((2,), "int64")
     dec = []
@@ -363,32 +416,53 @@ def sum_product_rate(a, pipe, rank, world, dist, steps=2):
         payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (700 + i)))
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record()
+        lb.qc_decode(llr, pipe.ldpc, a.iters, a.variant, 0.75, early_stop=False, ref_bits=payload,
+                     want_hard=False, counts=counts, precision=precision, prune=prune)
+        d1.record()
+        dec.append((d0, d1))
+
+    ms, clk = _timed_steps(one, steps, dist)
+    dms = sum(d0.elapsed_time(d1) for d0, d1 in dec[1:]) / steps
+    c = counts.cpu().tolist()
+    return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
+            "decoder_ms_per_launch": dms, "decoder_gbit_s": B * K_INFO / (dms / 1e3) / 1e9,
+            "dtype": "f16x2" if precision == "fp16x2" else "f32",
+            "rows": "24 live rows (dead extension rows pruned)" if prune else "all 46 rows",
+            "roofline_frac": B * _bytes_cw(a.iters) / (dms / 1e3) / 1e9 / float(_peaks().get("hbm_gbs", 6650.0)),
+            "bit_errors": c[0], "block_errors": c[1], "clocks": clk,
+            "note": "fast mode: Philox noise, f32 modem, narrower message arithmetic; statistically "
+                    "equivalent to the reference, not bit-exact"}
+
+
+def sum_product_rate(a, rank, world, dist, steps=2):
+    """The reference's default BP variant (sum-product, ldpc.py:139-143), fast
+    mode, fixed iterations: fp16 per-edge messages on chip, fp32 math."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+    from paper_2203_11854_b200 import _lib as L
+
+    pipe = _fast_pipe(a, "sum-product")
+    B = a.batch
+    counts = L.zeros((2,), "int64")
+    dec = []
+
+    def one(i):
+        payload, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, ((rank + 1) << 40) | (600 + i)))
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
         lb.qc_decode(llr, pipe.ldpc, a.iters, "sum-product", early_stop=False, ref_bits=payload, want_hard=False,
                      counts=counts)
         d1.record()
         dec.append((d0, d1))
 
-    one(-1)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    dec.clear()
-    counts.zero_()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(steps):
-        one(i)
-    e1.record()
-    torch.cuda.synchronize()
-    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    ms = float(tm[0])
+    ms, clk = _timed_steps(one, steps, dist)
+    dms = sum(d0.elapsed_time(d1) for d0, d1 in dec[1:]) / steps
     c = counts.cpu().tolist()
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
-            "decoder_ms_per_launch": sum(d0.elapsed_time(d1) for d0, d1 in dec) / steps,
-            "bit_errors": c[0], "block_errors": c[1], "blocks": world * B * steps,
-            "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi, product-domain check update)"}
+            "decoder_ms_per_launch": dms, "bit_errors": c[0], "block_errors": c[1], "clocks": clk,
+            "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi, "
+                    "product-domain check update); fast mode, statistically equivalent"}
 
 
 def _wall_max(dist, secs):
@@ -403,14 +477,12 @@ def _wall_max(dist, secs):
 
 def e2e_chain(a, pipe, rank, world, dist, steps=3):
     """The public API call a user makes (Pipeline.run_batch, sweep.py:347):
-    host numpy (payload, decoded) out every step."""
+    host numpy (payload, decoded) out every step; exact chain."""
     import torch
 
     import paper_2203_11854_b200 as lb
 
     B = a.batch
-    # two warm-up calls: the caller holds one result while the next is made, so
-    # the pinned-host caching allocator needs two output sets before steady state
     p, d = pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 98))
     p, d = pipe.run_batch(a.ebno, B, lb.RngStream(a.seed, 99))
     torch.cuda.synchronize()
@@ -426,9 +498,10 @@ def e2e_chain(a, pipe, rank, world, dist, steps=3):
             "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys"}
 
 
-def e2e_decode(a, pipe, rank, world, dist, steps=5):
-    """Drop-in decoder with HOST buffers: pinned f32 LLRs in, decoded bits out
-    (ldpc5g_decode(llr, code, mode='fast'))."""
+def e2e_decode(a, pipe, rank, world, dist, steps=3):
+    """The drop-in decoder with HOST buffers: pinned f32 LLRs in, decoded bits
+    out (ldpc5g_decode(llr, code), exact mode, ldpc.py:354-365): the H2D copy
+    of each step's LLRs and the D2H copy of its bits are inside the timed region."""
     import torch
 
     import paper_2203_11854_b200 as lb
@@ -438,41 +511,21 @@ def e2e_decode(a, pipe, rank, world, dist, steps=5):
     host = torch.empty(llr.shape, dtype=torch.float32, pin_memory=True)
     host.copy_(llr)
     del llr
-    out = torch.empty((B, K_INFO), dtype=torch.uint8, pin_memory=True)
-    for _ in range(3):  # steady state of the pinned-host caching allocator
-        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
+    for _ in range(2):  # steady state of the pinned-host caching allocator
+        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t = time.perf_counter()
     for _ in range(steps):
-        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="fast", early_stop=a.early_stop)
-        assert dec.device.type == "cpu" and dec.shape == out.shape  # decoded bits are on the host
+        dec = lb.ldpc5g_decode(host, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop)
+        assert dec.device.type == "cpu" and dec.shape == (B, K_INFO)  # decoded bits are on the host
     torch.cuda.synchronize()
     el = _wall_max(dist, time.perf_counter() - t)
     return {"value": world * B * K_INFO * steps / el / 1e9, "unit": "Gbit/s",
             "h2d_bytes_per_step": 4 * B * N_TX, "d2h_bytes_per_step": B * K_INFO,
-            "api": "ldpc5g_decode(pinned host f32 LLRs) -> host bits"}
-
-
-def exact_rate(a, pipe, B=1024):
-    """Throughput of the bit-exact (reference-arithmetic) decoder on a smaller batch."""
-    import torch
-
-    import paper_2203_11854_b200 as lb
-
-    _, llr = pipe._llr(a.ebno, B, lb.RngStream(a.seed, 55))
-    for _ in range(2):  # same batch size, so the workspace pool is warm
-        lb.ldpc5g_decode(llr, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    lb.ldpc5g_decode(llr, pipe.ldpc, a.iters, a.variant, mode="exact", early_stop=a.early_stop, device=True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    return {"value": B * K_INFO / (ms / 1e3) / 1e9, "unit": "Gbit/s", "batch": B,
-            "note": "exact mode = reference arithmetic, bit-identical min-sum"}
+            "api": "ldpc5g_decode(pinned host f32 LLRs, mode='exact') -> host bits (copies overlap the decoder "
+                   "in 2,048-row chunks)"}
 
 
 def main():

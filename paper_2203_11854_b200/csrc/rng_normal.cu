@@ -20,7 +20,9 @@
 
 #include <algorithm>
 
-#define LS_ZIG_QUAL static __constant__
+// global (L1-cached) rather than __constant__: every lane of a warp indexes
+// the tables with its own random level, which the constant cache serialises
+#define LS_ZIG_QUAL static __device__ const
 #include "common.cuh"
 #include "ziggurat_tables.h"
 
@@ -141,6 +143,38 @@ __device__ double zig_draw(uint64_t seed, uint64_t sid, int64_t p, int *len) {
   }
 }
 
+// sort the specials of a segment by position (thread 0; ~8 entries)
+__device__ __forceinline__ void zig_sort(uint16_t *spos, uint16_t *slen, double *sval, int n) {
+  for (int i = 1; i < n; ++i) {
+    const uint16_t p = spos[i], l = slen[i];
+    const double v = sval ? sval[i] : 0.0;
+    int j = i - 1;
+    while (j >= 0 && spos[j] > p) {
+      spos[j + 1] = spos[j];
+      slen[j + 1] = slen[j];
+      if (sval) sval[j + 1] = sval[j];
+      --j;
+    }
+    spos[j + 1] = p;
+    slen[j + 1] = l;
+    if (sval) sval[j + 1] = v;
+  }
+}
+
+// Multi-word ("special") draws of a segment, evaluated CONVERGED: the
+// positions are collected first, then one lane per special walks the slow
+// path, so a warp runs the wedge / tail code once instead of once per lane
+// that happens to hold a special word.
+__device__ __forceinline__ void zig_eval_specials(uint64_t seed, uint64_t sid, int64_t base, uint16_t *spos,
+                                                  uint16_t *slen, double *sval, int n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    int len;
+    const double v = zig_draw(seed, sid, base + spos[k], &len);
+    slen[k] = (uint16_t)min(len, 65535);
+    if (sval) sval[k] = v;
+  }
+}
+
 // specials of segment s (sorted by position), shared by the segment kernels
 __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *spos, uint16_t *slen,
                             int *count, int *overflow) {
@@ -156,33 +190,19 @@ __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *sp
       const uint64_t r = w[u] >> 8;
       const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
       if (!(rabs < ls_zig_ki[w[u] & 0xff])) {
-        int len;
-        zig_draw(seed, sid, base + 4 * b + u, &len);
         const int k = atomicAdd(count, 1);
-        if (k < kZSpec) {
+        if (k < kZSpec)
           spos[k] = (uint16_t)(4 * b + u);
-          slen[k] = (uint16_t)min(len, 65535);
-        } else {
+        else
           *overflow = 1;
-        }
       }
     }
   }
   __syncthreads();
   const int n = min(*count, kZSpec);
-  if (t == 0) {  // insertion sort, ~8 entries
-    for (int i = 1; i < n; ++i) {
-      const uint16_t p = spos[i], l = slen[i];
-      int j = i - 1;
-      while (j >= 0 && spos[j] > p) {
-        spos[j + 1] = spos[j];
-        slen[j + 1] = slen[j];
-        --j;
-      }
-      spos[j + 1] = p;
-      slen[j + 1] = l;
-    }
-  }
+  zig_eval_specials(seed, sid, base, spos, slen, nullptr, n);
+  __syncthreads();
+  if (t == 0) zig_sort(spos, slen, nullptr, n);
   __syncthreads();
   return n;
 }
@@ -282,6 +302,7 @@ __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, i
                                                   const int *__restrict__ sentry, const int64_t *__restrict__ sbase,
                                                   int64_t count, double *__restrict__ out, int *__restrict__ overflow) {
   __shared__ uint16_t spos[kZSpec], slen[kZSpec];
+  __shared__ double sval[kZSpec];
   __shared__ int cnt_s;
   const int t = threadIdx.x;
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
@@ -292,7 +313,7 @@ __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, i
     uint64_t w[4];
     philox4x64_10((uint64_t)(s * (kZG / 4) + t) + 1, 0, 0, 0, sid, seed, w);
     double val[4];
-    int len[4];
+    uint32_t spec = 0;  // bit u: word 4t+u starts a multi-word draw
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int idx = (int)(w[u] & 0xff);
@@ -300,47 +321,46 @@ __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, i
       const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
       double x = (double)rabs * ls_zig_wi[idx];
       if (r & 0x1) x = -x;
-      len[u] = 1;
       val[u] = x;
       if (!(rabs < ls_zig_ki[idx])) {
-        val[u] = zig_draw(seed, sid, s * kZG + 4 * t + u, &len[u]);
+        spec |= 1u << u;
         const int k = atomicAdd(&cnt_s, 1);
-        if (k < kZSpec) {
+        if (k < kZSpec)
           spos[k] = (uint16_t)(4 * t + u);
-          slen[k] = (uint16_t)min(len[u], 65535);
-        } else {
+        else
           *overflow = 1;
-        }
       }
     }
     __syncthreads();
     const int n = min(cnt_s, kZSpec);
-    if (t == 0) {
-      for (int a = 1; a < n; ++a) {
-        const uint16_t p = spos[a], l = slen[a];
-        int b = a - 1;
-        while (b >= 0 && spos[b] > p) {
-          spos[b + 1] = spos[b];
-          slen[b + 1] = slen[b];
-          --b;
-        }
-        spos[b + 1] = p;
-        slen[b + 1] = l;
-      }
-    }
+    zig_eval_specials(seed, sid, s * kZG, spos, slen, sval, n);
+    __syncthreads();
+    if (t == 0) zig_sort(spos, slen, sval, n);
     __syncthreads();
     const int e = sentry[s];
     int cnt, cur;
     zig_walk(spos, slen, n, e, 4 * t, &cnt, &cur);
+    // specials of this thread, in position order, are consecutive in the list
+    int k = 0;
+    if (spec) {
+      while (k < n && spos[k] < 4 * t) ++k;
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = 4 * t + u;
+      int len = 1;
+      double v = val[u];
+      if ((spec >> u) & 1u) {
+        len = slen[k];
+        v = sval[k];
+        ++k;
+      }
       if (p >= cur) {  // a draw starts here (cur >= e always)
         const int64_t j = base + cnt + (p - cur);
-        if (j < count) out[j] = val[u];
-        if (len[u] > 1) {  // multi-word draw: the next start is p + len
+        if (j < count) out[j] = v;
+        if (len > 1) {  // multi-word draw: the next start is p + len
           cnt += p - cur + 1;
-          cur = p + len[u];
+          cur = p + len;
         }
       }
     }

@@ -234,12 +234,15 @@ def ldpc5g_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "sum
     """BP-decode rate-matched LLRs -> [batch, k] info bits (ldpc.py:354-365)."""
     _check_variant(variant, num_iter)
     if mode == "exact":
-        t = L.to_device(llr)
-        if t.dim() == 1:
-            t = t.unsqueeze(0)
-        if (t.dtype == L.torch().float32 and variant != "sum-product"
-                and qc_has_kernel(code, precision="exact")):
+        f32_in = (llr.dtype == L.torch().float32) if L.is_tensor(llr) else (np.asarray(llr).dtype == np.float32)
+        if f32_in and variant != "sum-product" and qc_has_kernel(code, precision="exact"):
             # on-chip exact decoder with derate_match fused in
+            host_in = not L.is_tensor(llr) or not llr.is_cuda
+            if host_in and not device:
+                return _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, "exact")
+            t = L.to_device(llr)
+            if t.dim() == 1:
+                t = t.unsqueeze(0)
             out = qc_decode(t, code, num_iter, variant, scale, early_stop=early_stop,
                             precision="exact")["hard"]
             return L.to_host(out) if (not L.is_tensor(llr) and not device) else out

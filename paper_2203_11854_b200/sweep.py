@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 from . import _lib as L
 from .channel import awgn
 from .core import RngStream, binary_source, ebnodb2no
-from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode
+from .ldpc import BP_VARIANTS, LdpcCode5G, ldpc5g_decode, ldpc5g_encode, qc_decode, qc_has_kernel
 from .mapping import Constellation, demap_app, demap_maxlog, map_bits, modem_qam
 
 CSV_COLUMNS = ("ebno_db", "bits", "bit_errors", "ber", "blocks", "block_errors", "bler", "batches",
@@ -228,6 +228,15 @@ class Pipeline:
         return payload, llr
 
     @property
+    def qc_exact(self) -> bool:
+        """Exact mode served by the on-chip QC decoder (min-sum variants)."""
+        if self.family == "none" or self.decoder_mode != "exact":
+            return False
+        if getattr(self, "_qc_exact", None) is None:
+            self._qc_exact = qc_has_kernel(self.ldpc, precision="exact", variant=self.bp_variant)
+        return self._qc_exact
+
+    @property
     def precision(self) -> str:
         if self.decoder_precision != "auto":
             return self.decoder_precision
@@ -279,11 +288,12 @@ class Pipeline:
         device int64[2] `counts` without any host synchronisation."""
         if counts is None:
             counts = L.zeros((2,), "int64")
-        if self.family != "none" and self.decoder_mode == "fast":
+        if self.family != "none" and (self.decoder_mode == "fast" or self.qc_exact):
+            # decoder with derate, hard decision and error counting fused
             payload, llr = self._llr(ebno_db, batch_size, rng)
             qc_decode(llr, self.ldpc, self.bp_iter, self.bp_variant, self.bp_scale,
                       early_stop=self.bp_early_stop, ref_bits=payload, want_hard=False, counts=counts,
-                      precision=self.precision)
+                      precision="exact" if self.decoder_mode == "exact" else self.precision)
             return counts
         p, d = self.run_batch_device(ebno_db, batch_size, rng)
         L.call("ls_count_errors", L.ptr(p), L.ptr(d), p.shape[0], p.shape[1], L.ptr(counts), L.stream_ptr())

@@ -15,6 +15,7 @@ p.add_argument("--n", type=int, default=16896)
 p.add_argument("--m", type=int, default=4)
 p.add_argument("--ebno", type=float, default=6.0)
 p.add_argument("--noise", default="philox", choices=["philox", "numpy"])
+p.add_argument("--decoder", default="fp16x2", choices=["fp16x2", "fp32", "exact"])
 a = p.parse_args()
 code = lb.LdpcCode5G(a.k, a.n)
 const = lb.Constellation("qam", a.m)
@@ -35,7 +36,8 @@ def run(timed):
     ev[4].record()
     llr = lb.demap_app(y, no, const, out_dtype="float32", device=True)
     ev[5].record()
-    res = lb.qc_decode(llr, code, 20, "min-sum", early_stop=False, ref_bits=bits, want_hard=False)
+    res = lb.qc_decode(llr, code, 20, "min-sum", early_stop=False, ref_bits=bits, want_hard=False,
+                       precision=a.decoder)
     ev[6].record()
     torch.cuda.synchronize()
     if timed:
