@@ -95,13 +95,33 @@ struct QxGeo {
     while (r < MB && G::row_start[r] * NTL < tot * g) ++r;
     return r;
   }
+  // variable-node work of core column c in instructions (~13 per edge plus
+  // the per-column channel load, sum and store), for balancing the groups
+  static constexpr int ccost(int c) { return 13 * cdeg(c) + 16; }
   static constexpr int cfirst(int g) {
     if (g <= 0) return 0;
     if (g >= NTL) return KBC;
-    const int tot = G::col_start[KBC];
-    int c = 0;
-    while (c < KBC && G::col_start[c] * NTL < tot * g) ++c;
+    int tot = 0;
+    for (int c = 0; c < KBC; ++c) tot += ccost(c);
+    int c = 0, acc = 0;
+    while (c < KBC && acc * NTL < tot * g) acc += ccost(c++);
     return c;
+  }
+  // variable-node columns are processed in pairs (two independent gather /
+  // sum chains interleaved) when their degrees sum to at most VPAIR
+  static constexpr int VPAIR = 0;
+  static constexpr int vkind(int c) {  // 0 single, 1 first of a pair, 2 second of a pair
+    int g = 0;
+    while (g + 1 < NTL && c >= cfirst(g + 1)) ++g;
+    const int end = cfirst(g + 1);
+    int q = cfirst(g);
+    while (q < end) {
+      const bool pair = q + 1 < end && cdeg(q) + cdeg(q + 1) <= VPAIR;
+      if (q == c) return pair ? 1 : 0;
+      if (pair && q + 1 == c) return 2;
+      q += pair ? 2 : 1;
+    }
+    return 0;
   }
   // thread group owning row r / core column c (compile-time only: the
   // tables are host constexpr arrays)
@@ -155,6 +175,36 @@ __device__ __forceinline__ float qx_clip(float x) { return fminf(fmaxf(x, -40.0f
 // or the mother LLRs themselves (bp_decode on the code's pcm)
 __device__ __forceinline__ float qx_chan(const QcChanParams &P, const float *__restrict__ row, int v, bool mother) {
   return mother ? -__ldg(row + v) : chan_value(P, row, v);
+}
+
+// gather the messages into core column c at lane j (ascending check order):
+// c2v = +-(alpha*min1 | alpha*min2) from the compressed state of each check
+template <class Geo, int c>
+__device__ __forceinline__ void qx_vn_gather(double *x, uint32_t j8, const unsigned char *qx_sm, const double *m2) {
+  using G = typename Geo::G;
+  constexpr int Z = Geo::Z, d = Geo::cdeg(c), cs = G::col_start[c];
+  sfor<0, d>([&](auto tc) {
+    constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
+    constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
+    using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+    uint32_t o8 = j8 - 8u * s;  // 8 * ((j - s) mod Z)
+    o8 = min(o8, o8 + 8u * Z);
+    const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
+    double mag;
+    if ((w >> D) == (uint32_t)p)
+      mag = *reinterpret_cast<const double *>(reinterpret_cast<const char *>(m2) + 8 * r * Z + o8);
+    else
+      mag = *reinterpret_cast<const double *>(qx_sm + 8 * r * Z + o8);
+    x[q] = qx_flip(mag, (w << (32 - D + p)) & 0x80000000u);
+  });
+}
+
+// total = clip(f32(f64(chan) + (x0 + pairwise(x1..))), +-40)
+template <int d>
+__device__ __forceinline__ float qx_vn_total(const double *x, float ch) {
+  double sum = x[0];
+  if constexpr (d > 1) sum = __dadd_rn(x[0], qx_pairwise<d - 1>(x + 1));
+  return qx_clip(__double2float_rn(__dadd_rn((double)ch, sum)));
 }
 
 template <class Geo, bool ES, bool OUT>
@@ -276,26 +326,20 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         sfor<0, KBC>([&](auto cc) {
           constexpr int c = decltype(cc)::value;
           if (grp != Geo::cowner(c)) return;  // warp-uniform
-          constexpr int d = Geo::cdeg(c), cs = G::col_start[c];
-          const float ch = chn[c * Z + j];
-          double x[d];
-          sfor<0, d>([&](auto tc) {
-            constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
-            constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
-            using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
-            uint32_t o8 = j8 - 8u * s;  // 8 * ((j - s) mod Z)
-            o8 = min(o8, o8 + 8u * Z);
-            const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
-            double mag;
-            if ((w >> D) == (uint32_t)p)
-              mag = *reinterpret_cast<const double *>(reinterpret_cast<const char *>(m2) + 8 * r * Z + o8);
-            else
-              mag = *reinterpret_cast<const double *>(qx_sm + 8 * r * Z + o8);
-            x[q] = qx_flip(mag, (w << (32 - D + p)) & 0x80000000u);
-          });
-          double sum = x[0];
-          if constexpr (d > 1) sum = __dadd_rn(x[0], qx_pairwise<d - 1>(x + 1));
-          T[c * Z + j] = qx_clip(__double2float_rn(__dadd_rn((double)ch, sum)));
+          constexpr int kind = Geo::vkind(c);
+          if constexpr (kind == 0) {
+            const float ch = chn[c * Z + j];
+            double x[Geo::cdeg(c)];
+            qx_vn_gather<Geo, c>(x, j8, qx_sm, m2);
+            T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x, ch);
+          } else if constexpr (kind == 1) {  // columns c and c+1 interleaved
+            const float ch0 = chn[c * Z + j], ch1 = chn[(c + 1) * Z + j];
+            double x0[Geo::cdeg(c)], x1[Geo::cdeg(c + 1)];
+            qx_vn_gather<Geo, c>(x0, j8, qx_sm, m2);
+            qx_vn_gather<Geo, c + 1>(x1, j8, qx_sm, m2);
+            T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x0, ch0);
+            T[(c + 1) * Z + j] = qx_vn_total<Geo::cdeg(c + 1)>(x1, ch1);
+          }
         });
       }
       __syncthreads();
