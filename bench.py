@@ -298,7 +298,7 @@ def run_b200(a, rank, world, local_rank):
     if not a.no_extra:
         line["exact_early_stop"] = exact_early_stop_rate(a, pipe, rank, world, dist)
         line["fast_fp16x2_min_sum"] = fast_rate(a, rank, world, dist, "fp16x2", prune=True)
-        line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32", prune=False)
+        line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32-full", prune=False)
         line["sum_product_fast"] = sum_product_rate(a, rank, world, dist)
     if rank == 0 and world == 1 and not a.no_cpu:
         v, cw, el = cpu_chain_rate(a, a.cpu_seconds, os.cpu_count() or 1)
@@ -427,6 +427,7 @@ def fast_rate(a, rank, world, dist, precision, prune, steps=3):
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
             "decoder_ms_per_launch": dms, "decoder_gbit_s": B * K_INFO / (dms / 1e3) / 1e9,
             "dtype": "f16x2" if precision == "fp16x2" else "f32",
+            "kernel": {"fp16x2": "k_qc_fast_h2w", "fp32-full": "k_qc_exact<BG1,384,2,float>"}.get(precision, precision),
             "rows": "24 live rows (dead extension rows pruned)" if prune else "all 46 rows",
             "roofline_frac": B * _bytes_cw(a.iters) / (dms / 1e3) / 1e9 / float(_peaks().get("hbm_gbs", 6650.0)),
             "bit_errors": c[0], "block_errors": c[1], "clocks": clk,

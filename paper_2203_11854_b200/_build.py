@@ -68,14 +68,16 @@ def _instance_sources():
                 "}\n}  // namespace lsb\n")
         out.append(_write(f"qcsprt_{bg}_{rb}_{sp}.cu", body))
     for bg, z, ntl in re.findall(r"V\((\d+),\s*(\d+),\s*(\d+)\)", text):
-        body = (f'#include "{CSRC}/bp_qc_exact.cuh"\n'
-                "namespace lsb {\n"
-                f"int qcx_{bg}_{z}(const QcChanParams &P, const float *l, int64_t B, int it, double a, int es, int mo,\n"
-                "    uint8_t *h, int hl, float *lo, int32_t *iu, const uint8_t *ref, unsigned long long *cnt,\n"
-                "    cudaStream_t s) {\n"
-                f"  return launch_qc_exact<BG{bg}Tables, {z}, {ntl}>(P, l, B, it, a, es, mo, h, hl, lo, iu, ref, cnt, s);\n"
-                "}\n}  // namespace lsb\n")
-        out.append(_write(f"qcx_{bg}_{z}.cu", body))
+        for mt, tag in (("double", "qcx"), ("float", "qcf")):
+            body = (f'#include "{CSRC}/bp_qc_exact.cuh"\n'
+                    "namespace lsb {\n"
+                    f"int {tag}_{bg}_{z}(const QcChanParams &P, const float *l, int64_t B, int it, double a, int es,\n"
+                    "    int mo, uint8_t *h, int hl, float *lo, int32_t *iu, const uint8_t *ref,\n"
+                    "    unsigned long long *cnt, cudaStream_t s) {\n"
+                    f"  return launch_qc_exact<BG{bg}Tables, {z}, {ntl}, {mt}>(P, l, B, it, a, es, mo, h, hl, lo, iu, ref,\n"
+                    "                                                          cnt, s);\n"
+                    "}\n}  // namespace lsb\n")
+            out.append(_write(f"{tag}_{bg}_{z}.cu", body))
     return out
 
 

@@ -250,13 +250,16 @@ typedef int (*QcxFn)(const QcChanParams &, const float *, int64_t, int, double, 
                      int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
 #define LSB_QCX_DECL(bg, z, ntl)                                                                              \
   int qcx_##bg##_##z(const QcChanParams &, const float *, int64_t, int, double, int, int, uint8_t *, int, float *, \
+                     int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);                          \
+  int qcf_##bg##_##z(const QcChanParams &, const float *, int64_t, int, double, int, int, uint8_t *, int, float *, \
                      int32_t *, const uint8_t *, unsigned long long *, cudaStream_t);
 LSB_QCX_INSTANCES(LSB_QCX_DECL)
 struct QcxEntry {
   int bg, z;
-  QcxFn fn;
+  QcxFn fn;   // f64 messages: exact
+  QcxFn fn32; // f32 messages: fp32 full-graph fast mode
 };
-#define LSB_QCX_ENTRY(bg, z, ntl) {bg, z, &qcx_##bg##_##z},
+#define LSB_QCX_ENTRY(bg, z, ntl) {bg, z, &qcx_##bg##_##z, &qcf_##bg##_##z},
 static const QcxEntry kQcxKernels[] = {LSB_QCX_INSTANCES(LSB_QCX_ENTRY)};
 
 static const QcxEntry *find_qcx(const ls_code *code) {
@@ -301,7 +304,7 @@ extern "C" int ls_qc_has_kernel(const ls_code *code, int flags) {
   if (!code) return 0;
   const int R = (flags & LS_QC_PRUNE) ? live_rows(code->p) : code->p.mb;
   const int prec = (flags & LS_QC_SP) ? 2 : qc_kind(LS_MIN_SUM, flags);
-  if (flags & LS_QC_EXACT) return find_qcx(code) != nullptr;
+  if (flags & (LS_QC_EXACT | LS_QC_FULL32)) return find_qcx(code) != nullptr;
   if (!code->std_shifts) return 0;
   for (const QcKernelEntry &k : kQcKernels)
     if (k.bg == code->p.bg && k.z == code->p.z && k.r == R && k.prec == prec) return 1;
@@ -319,16 +322,17 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   const QcParams &P = code->p;
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
-  if (flags & LS_QC_EXACT) {
+  if (flags & (LS_QC_EXACT | LS_QC_FULL32)) {
     if (variant == LS_SUM_PRODUCT)
-      return fail(LS_EINVAL, "ls_qc_decode: the on-chip exact decoder serves min-sum and scaled-min-sum; "
-                             "use ls_bp_decode for sum-product");
+      return fail(LS_EINVAL, "ls_qc_decode: the on-chip exact / fp32 full-graph decoder serves min-sum and "
+                             "scaled-min-sum; use ls_bp_decode for sum-product");
     const QcxEntry *k = find_qcx(code);
     if (!k) return fail(LS_EINVAL, "ls_qc_decode: no on-chip exact decoder instance for this code");
     const QcChanParams CP{P.z, P.k, P.n, P.k_full, P.n_full, P.l1, P.buflen};
     const int mother = (flags & LS_QC_MOTHER) ? 1 : 0;
-    return k->fn(CP, llr, batch, num_iter, variant == LS_SCALED_MIN_SUM ? scale : 1.0, early_stop, mother, hard_k,
-                 mother ? P.n_full : P.k, llr_out, iters_used, ref_bits, counts, s);
+    const QcxFn fn = (flags & LS_QC_EXACT) ? k->fn : k->fn32;
+    return fn(CP, llr, batch, num_iter, variant == LS_SCALED_MIN_SUM ? scale : 1.0, early_stop, mother, hard_k,
+              mother ? P.n_full : P.k, llr_out, iters_used, ref_bits, counts, s);
   }
   const int prec = qc_kind(variant, flags);
   const int R = (flags & LS_QC_PRUNE) ? live_rows(P) : P.mb;

@@ -57,9 +57,14 @@
 
 namespace lsb {
 
-template <class G_, int Z_, int NTL_>
+// M = double: the EXACT decoder (reference arithmetic); M = float: the fp32
+// full-graph fast decoder (same schedule and layout with f32 messages, so
+// min2 fits in shared memory too)
+template <class G_, int Z_, int NTL_, class M_ = double>
 struct QxGeo {
   using G = G_;
+  using M = M_;
+  static constexpr bool EXACT = sizeof(M_) == 8;
   static constexpr int Z = Z_, NTL = NTL_;
   static constexpr int NT1 = ((Z + 31) / 32) * 32, NT = NT1 * NTL;
   static constexpr int MB = G::MB, NB = G::NB, KBC = G::KB + 4, NEXT = G::NB - (G::KB + 4);
@@ -73,8 +78,11 @@ struct QxGeo {
     return b;
   }
   static constexpr int wbytes(int r) { return deg(r) + argbits(deg(r)) <= 16 ? 2 : 4; }
+  // shared: M1 [MB][Z] M, (fp32: M2 [MB][Z] M), W, T
+  static constexpr int M2_OFF = (int)sizeof(M_) * MB * Z;
+  static constexpr int W_OFF = EXACT ? M2_OFF : 2 * M2_OFF;
   static constexpr int woff(int r) {  // byte offset of row r's word array
-    int o = 8 * MB * Z;
+    int o = W_OFF;
     for (int q = 0; q < r; ++q) {
       if (wbytes(q) == 4) o = (o + 3) & ~3;
       o += wbytes(q) * Z;
@@ -107,22 +115,6 @@ struct QxGeo {
     while (c < KBC && acc * NTL < tot * g) acc += ccost(c++);
     return c;
   }
-  // variable-node columns are processed in pairs (two independent gather /
-  // sum chains interleaved) when their degrees sum to at most VPAIR
-  static constexpr int VPAIR = 0;
-  static constexpr int vkind(int c) {  // 0 single, 1 first of a pair, 2 second of a pair
-    int g = 0;
-    while (g + 1 < NTL && c >= cfirst(g + 1)) ++g;
-    const int end = cfirst(g + 1);
-    int q = cfirst(g);
-    while (q < end) {
-      const bool pair = q + 1 < end && cdeg(q) + cdeg(q + 1) <= VPAIR;
-      if (q == c) return pair ? 1 : 0;
-      if (pair && q + 1 == c) return 2;
-      q += pair ? 2 : 1;
-    }
-    return 0;
-  }
   // thread group owning row r / core column c (compile-time only: the
   // tables are host constexpr arrays)
   static constexpr int rowner(int r) {
@@ -137,34 +129,46 @@ struct QxGeo {
   }
 };
 
-// x with its sign bit flipped when `bit` is 1 (c2v = (-alpha)*excl)
+// x with its sign bit flipped when `bit31` is 0x80000000 (c2v = (-alpha)*excl)
 __device__ __forceinline__ double qx_flip(double x, uint32_t bit31) {
   return __hiloint2double(__double2hiint(x) ^ (int)bit31, __double2loint(x));
 }
+__device__ __forceinline__ float qx_flip(float x, uint32_t bit31) {
+  return __uint_as_float(__float_as_uint(x) ^ bit31);
+}
+__device__ __forceinline__ double qx_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float qx_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double qx_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float qx_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double qx_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float qx_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ uint32_t qx_hi(double x) { return (uint32_t)__double2hiint(x); }
+__device__ __forceinline__ uint32_t qx_hi(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ float qx_to_f32(double x) { return __double2float_rn(x); }
+__device__ __forceinline__ float qx_to_f32(float x) { return x; }
 
 // numpy pairwise_sum of N compile-time terms (loops_utils.h.src): fewer
 // than 8 terms sequentially from -0.0, else 8 strided accumulators, their
 // tree, then the remainder in order
-template <int N>
-__device__ __forceinline__ double qx_pairwise(const double *x) {
+template <int N, class M>
+__device__ __forceinline__ M qx_pairwise(const M *x) {
   if constexpr (N < 8) {
-    double r = -0.0;
+    M r = (M)-0.0;
 #pragma unroll
-    for (int q = 0; q < N; ++q) r = __dadd_rn(r, x[q]);
+    for (int q = 0; q < N; ++q) r = qx_add(r, x[q]);
     return r;
   } else {
-    double r[8];
+    M r[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) r[q] = x[q];
     constexpr int NB8 = N - N % 8;
 #pragma unroll
     for (int q = 8; q < NB8; q += 8)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] = __dadd_rn(r[u], x[q + u]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (int u = 0; u < 8; ++u) r[u] = qx_add(r[u], x[q + u]);
+    M res = qx_add(qx_add(qx_add(r[0], r[1]), qx_add(r[2], r[3])), qx_add(qx_add(r[4], r[5]), qx_add(r[6], r[7])));
 #pragma unroll
-    for (int q = NB8; q < N; ++q) res = __dadd_rn(res, x[q]);
+    for (int q = NB8; q < N; ++q) res = qx_add(res, x[q]);
     return res;
   }
 }
@@ -180,9 +184,11 @@ __device__ __forceinline__ float qx_chan(const QcChanParams &P, const float *__r
 // gather the messages into core column c at lane j (ascending check order):
 // c2v = +-(alpha*min1 | alpha*min2) from the compressed state of each check
 template <class Geo, int c>
-__device__ __forceinline__ void qx_vn_gather(double *x, uint32_t j8, const unsigned char *qx_sm, const double *m2) {
+__device__ __forceinline__ void qx_vn_gather(typename Geo::M *x, uint32_t j8, const unsigned char *qx_sm,
+                                             const typename Geo::M *m2) {
   using G = typename Geo::G;
-  constexpr int Z = Geo::Z, d = Geo::cdeg(c), cs = G::col_start[c];
+  using M = typename Geo::M;
+  constexpr int Z = Geo::Z, d = Geo::cdeg(c), cs = G::col_start[c], SZ = (int)sizeof(M);
   sfor<0, d>([&](auto tc) {
     constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
     constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
@@ -190,21 +196,26 @@ __device__ __forceinline__ void qx_vn_gather(double *x, uint32_t j8, const unsig
     uint32_t o8 = j8 - 8u * s;  // 8 * ((j - s) mod Z)
     o8 = min(o8, o8 + 8u * Z);
     const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
-    double mag;
-    if ((w >> D) == (uint32_t)p)
-      mag = *reinterpret_cast<const double *>(reinterpret_cast<const char *>(m2) + 8 * r * Z + o8);
-    else
-      mag = *reinterpret_cast<const double *>(qx_sm + 8 * r * Z + o8);
+    const uint32_t oM = SZ == 8 ? o8 : (o8 >> 1);  // byte offset of check (r, i) in an [MB][Z] M array
+    M mag;
+    if ((w >> D) == (uint32_t)p) {
+      if constexpr (Geo::EXACT)
+        mag = *reinterpret_cast<const M *>(reinterpret_cast<const char *>(m2) + SZ * r * Z + oM);
+      else
+        mag = *reinterpret_cast<const M *>(qx_sm + Geo::M2_OFF + SZ * r * Z + oM);
+    } else {
+      mag = *reinterpret_cast<const M *>(qx_sm + SZ * r * Z + oM);
+    }
     x[q] = qx_flip(mag, (w << (32 - D + p)) & 0x80000000u);
   });
 }
 
-// total = clip(f32(f64(chan) + (x0 + pairwise(x1..))), +-40)
-template <int d>
-__device__ __forceinline__ float qx_vn_total(const double *x, float ch) {
-  double sum = x[0];
-  if constexpr (d > 1) sum = __dadd_rn(x[0], qx_pairwise<d - 1>(x + 1));
-  return qx_clip(__double2float_rn(__dadd_rn((double)ch, sum)));
+// total = clip(f32(chan + (x0 + pairwise(x1..))), +-40)
+template <int d, class M>
+__device__ __forceinline__ float qx_vn_total(const M *x, float ch) {
+  M sum = x[0];
+  if constexpr (d > 1) sum = qx_add(x[0], qx_pairwise<d - 1>(x + 1));
+  return qx_clip(qx_to_f32(qx_add((M)ch, sum)));
 }
 
 template <class Geo, bool ES, bool OUT>
@@ -213,17 +224,20 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
                int mother, uint8_t *__restrict__ hard, int hard_len, float *__restrict__ llr_out,
                int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref,
                unsigned long long *__restrict__ counts, unsigned long long *__restrict__ next,
-               double *__restrict__ m2ws, float *__restrict__ extws, float *__restrict__ chws) {
+               typename Geo::M *__restrict__ m2ws, float *__restrict__ extws, float *__restrict__ chws) {
   using G = typename Geo::G;
+  using M = typename Geo::M;
   constexpr int Z = Geo::Z, NT1 = Geo::NT1, NT = Geo::NT, MB = Geo::MB, KBC = Geo::KBC;
   extern __shared__ __align__(16) unsigned char qx_sm[];
-  double *M1 = reinterpret_cast<double *>(qx_sm);
+  M *M1 = reinterpret_cast<M *>(qx_sm);
+  // min2 per check: an L2 slice per CTA for f64 messages, shared memory for f32
+  M *m2 = Geo::EXACT ? m2ws + (size_t)blockIdx.x * MB * Z : reinterpret_cast<M *>(qx_sm + Geo::M2_OFF);
+  const M al = (M)alpha;
   float *T = reinterpret_cast<float *>(qx_sm + Geo::T_OFF);
   __shared__ long long cur;
   __shared__ unsigned red[NT / 32];
   const int t = threadIdx.x, grp = t / NT1, ln = t - grp * NT1;
   const bool lane = ln < Z;
-  double *m2 = m2ws + (size_t)blockIdx.x * MB * Z;
   float *ext = OUT ? extws + (size_t)blockIdx.x * Geo::NEXT * Z : nullptr;
   // channel values -derate(llr) of the current codeword, formed once per
   // codeword (fillers, punctured positions, repetitions) and re-read from L2
@@ -264,7 +278,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
           WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
           const int ci = r * Z + ln;
-          double m1o = 0.0, m2o = 0.0;
+          M m1o = 0, m2o = 0;
           uint32_t wo = 0u;
           if (!first) {
             m1o = M1[ci];
@@ -272,14 +286,14 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             wo = (uint32_t)W[ln];
           }
           const uint32_t argo = wo >> D;
-          double mn1 = INFINITY, mn2 = INFINITY;
+          M mn1 = (M)INFINITY, mn2 = (M)INFINITY;
           uint32_t arg = 0, sg = 0, syn = 0;
           sfor<0, D>([&](auto pc) {
             constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
             // old message on this edge: +-(alpha*min1 | alpha*min2), sign
             // bit of position p at bit D-1-p of the word
-            const double mag = argo == (uint32_t)p ? m2o : m1o;
-            const double cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
+            const M mag = argo == (uint32_t)p ? m2o : m1o;
+            const M cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
             uint32_t o = i4 + 4u * s;  // byte offset of lane (i + s) mod Z
             o = min(o, o - 4u * Z);
             float tv;
@@ -289,23 +303,30 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
               // degree-1 extension VN: its posterior is chan + its only message
               const int v = c * Z + (int)(o >> 2);
               const float ch = chn[v];
-              tv = first ? ch : qx_clip(__double2float_rn(__dadd_rn((double)ch, cold)));
+              tv = first ? ch : qx_clip(qx_to_f32(qx_add((M)ch, cold)));
               if (OUT && ES) ext[v - KBC * Z] = tv;
             }
             if (ES) syn ^= __float_as_uint(tv);
-            const double x = __dsub_rn((double)tv, cold);
-            const double a = fabs(x);
-            const bool lt1 = a < mn1, lt2 = a < mn2;
-            const double t2 = lt2 ? a : mn2;
-            mn2 = lt1 ? mn1 : t2;
-            mn1 = lt1 ? a : mn1;
-            arg = lt1 ? (uint32_t)p : arg;
-            sg = __funnelshift_l((uint32_t)__double2hiint(x), sg, 1);  // signbit(x) in at bit 0
+            const M x = qx_sub((M)tv, cold);
+            if constexpr (Geo::EXACT) {
+              const double a = fabs(x);
+              const bool lt1 = a < mn1, lt2 = a < mn2;
+              const double t2 = lt2 ? a : mn2;
+              mn2 = lt1 ? mn1 : t2;
+              mn1 = lt1 ? a : mn1;
+              arg = lt1 ? (uint32_t)p : arg;
+            } else {  // one FMNMX per update in f32
+              const float a = fabsf(x);
+              arg = a < mn1 ? (uint32_t)p : arg;
+              mn2 = fminf(mn2, fmaxf(mn1, a));
+              mn1 = fminf(mn1, a);
+            }
+            sg = __funnelshift_l(qx_hi(x), sg, 1);  // signbit(x) in at bit 0
           });
           bad |= syn >> 31;
           const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
-          M1[ci] = __dmul_rn(alpha, mn1);
-          m2[ci] = __dmul_rn(alpha, mn2);
+          M1[ci] = qx_mul(al, mn1);
+          m2[ci] = qx_mul(al, mn2);
           W[ln] = (WT)(osg | (arg << D));
         });
       }
@@ -326,20 +347,10 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         sfor<0, KBC>([&](auto cc) {
           constexpr int c = decltype(cc)::value;
           if (grp != Geo::cowner(c)) return;  // warp-uniform
-          constexpr int kind = Geo::vkind(c);
-          if constexpr (kind == 0) {
-            const float ch = chn[c * Z + j];
-            double x[Geo::cdeg(c)];
-            qx_vn_gather<Geo, c>(x, j8, qx_sm, m2);
-            T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x, ch);
-          } else if constexpr (kind == 1) {  // columns c and c+1 interleaved
-            const float ch0 = chn[c * Z + j], ch1 = chn[(c + 1) * Z + j];
-            double x0[Geo::cdeg(c)], x1[Geo::cdeg(c + 1)];
-            qx_vn_gather<Geo, c>(x0, j8, qx_sm, m2);
-            qx_vn_gather<Geo, c + 1>(x1, j8, qx_sm, m2);
-            T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x0, ch0);
-            T[(c + 1) * Z + j] = qx_vn_total<Geo::cdeg(c + 1)>(x1, ch1);
-          }
+          const float ch = chn[c * Z + j];
+          M x[Geo::cdeg(c)];
+          qx_vn_gather<Geo, c>(x, j8, qx_sm, m2);
+          T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x, ch);
         });
       }
       __syncthreads();
@@ -358,12 +369,12 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
             const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
             const uint32_t w = W[i];
-            const double mag = (w >> D) == (uint32_t)(D - 1) ? m2[r * Z + i] : M1[r * Z + i];
-            const double cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
+            const M mag = (w >> D) == (uint32_t)(D - 1) ? m2[r * Z + i] : M1[r * Z + i];
+            const M cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
             int j = i + s;
             j = j >= Z ? j - Z : j;
             const float ch = chn[c * Z + j];
-            ext[(c - KBC) * Z + j] = qx_clip(__double2float_rn(__dadd_rn((double)ch, cv)));
+            ext[(c - KBC) * Z + j] = qx_clip(qx_to_f32(qx_add((M)ch, cv)));
           }
         });
       }
@@ -401,13 +412,15 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
   }
 }
 
-// one exact-decoder instance: persistent grid, one L2 slice of min2 per CTA
-template <class G, int Z, int NTL>
+// one decoder instance: persistent grid; the exact (f64) decoder keeps an L2
+// slice of min2 per CTA, the fp32 one keeps everything but the channel in
+// shared memory
+template <class G, int Z, int NTL, class M = double>
 int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_iter, double alpha, int early_stop,
                     int mother, uint8_t *hard, int hard_len, float *llr_out, int32_t *iters_used, const uint8_t *ref,
                     unsigned long long *counts, cudaStream_t s) {
-  using Geo = QxGeo<G, Z, NTL>;
-  static_assert(Geo::SMEM <= 227 * 1024, "exact decoder state does not fit in shared memory");
+  using Geo = QxGeo<G, Z, NTL, M>;
+  static_assert(Geo::SMEM <= 227 * 1024, "decoder state does not fit in shared memory");
   const bool out = llr_out != nullptr || hard_len > Geo::KBC * Z;
   auto kern = early_stop ? (out ? k_qc_exact<Geo, true, true> : k_qc_exact<Geo, true, false>)
                          : (out ? k_qc_exact<Geo, false, true> : k_qc_exact<Geo, false, false>);
@@ -419,7 +432,7 @@ int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Geo::NT, Geo::SMEM);
   const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), B);
   if (grid <= 0) return LS_OK;
-  const size_t m2_bytes = sizeof(double) * (size_t)grid * Geo::MB * Z;
+  const size_t m2_bytes = Geo::EXACT ? sizeof(M) * (size_t)grid * Geo::MB * Z : 0;
   const size_t ext_bytes = out ? sizeof(float) * (size_t)grid * Geo::NEXT * Z : 0;
   const size_t ch_bytes = sizeof(float) * (size_t)grid * Geo::NB * Z;
   char *ws = nullptr;
@@ -428,7 +441,7 @@ int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(exact workspace)");
   unsigned long long *next = reinterpret_cast<unsigned long long *>(ws);
   cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
-  double *m2 = reinterpret_cast<double *>(ws + 256);
+  M *m2 = reinterpret_cast<M *>(ws + 256);
   float *ext = out ? reinterpret_cast<float *>(ws + 256 + m2_bytes) : nullptr;
   float *chn = reinterpret_cast<float *>(ws + 256 + m2_bytes + ext_bytes);
   kern<<<(unsigned)grid, Geo::NT, Geo::SMEM, s>>>(P, llr, B, num_iter, alpha, mother, hard, hard_len, llr_out,

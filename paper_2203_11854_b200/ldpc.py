@@ -296,7 +296,7 @@ def _decode_host_pipelined(llr, code, num_iter, variant, scale, early_stop, prec
     return out.numpy() if not L.is_tensor(llr) else out
 
 
-LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP, LS_QC_EXACT, LS_QC_MOTHER = 1, 2, 4, 8, 16, 32
+LS_QC_PRUNE, LS_QC_GENERIC, LS_QC_FP16, LS_QC_SP, LS_QC_EXACT, LS_QC_MOTHER, LS_QC_FULL32 = 1, 2, 4, 8, 16, 32, 64
 
 
 def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
@@ -305,7 +305,7 @@ def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
     (the sum-product fast decoder exists only as such instances; min-sum codes
     without one run the runtime-geometry fp16x2 or the runtime-Z fp32 kernel).
     precision "exact" asks for the on-chip exact decoder (min-sum variants)."""
-    if precision == "exact":
+    if precision in ("exact", "fp32-full"):
         return variant != "sum-product" and bool(L.lib().ls_qc_has_kernel(code.handle, LS_QC_EXACT))
     flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
     if variant == "sum-product":
@@ -327,19 +327,20 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
     the runtime-geometry kernel of that precision instead of a compile-time
     specialised instance.  precision "exact" is the on-chip bit-exact decoder
     (bp_qc_exact.cuh: whole mother graph, reference arithmetic; min-sum and
-    scaled-min-sum); with mother=True its input is mother LLRs [B, n_full]
+    scaled-min-sum) and "fp32-full" the same decoder with f32 messages (fast
+    mode, all rows); with mother=True the input is mother LLRs [B, n_full]
     and `hard` covers all n_full positions (bp_decode on code.pcm)."""
-    if precision not in ("fp32", "fp16x2", "exact"):
+    if precision not in ("fp32", "fp16x2", "exact", "fp32-full"):
         raise ValueError(f"unknown decoder precision {precision!r}")
-    if mother and precision != "exact":
-        raise ValueError("mother-length input needs precision='exact'")
-    if precision == "exact":
+    if mother and precision not in ("exact", "fp32-full"):
+        raise ValueError("mother-length input needs precision='exact' or 'fp32-full'")
+    if precision in ("exact", "fp32-full"):
         prune = False
     elif prune is None:
         prune = not want_llr
     flags = ((LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
              | (LS_QC_FP16 if precision == "fp16x2" else 0) | (LS_QC_EXACT if precision == "exact" else 0)
-             | (LS_QC_MOTHER if mother else 0))
+             | (LS_QC_FULL32 if precision == "fp32-full" else 0) | (LS_QC_MOTHER if mother else 0))
     _check_variant(variant, num_iter)
     t = L.to_device(llr, "float32")
     if t.dim() == 1:

@@ -43,17 +43,19 @@ def timed(fn, reps):
     return e0.elapsed_time(e1) / reps, out
 
 
-for variant in ("min-sum", "scaled-min-sum"):
-    for es in (False, True):
+for prec, variant, es in (("exact", "min-sum", False), ("exact", "min-sum", True), ("exact", "scaled-min-sum", False),
+                          ("exact", "scaled-min-sum", True), ("fp32-full", "min-sum", False),
+                          ("fp32-full", "min-sum", True)):
+    if True:
         counts = torch.zeros(2, dtype=torch.int64, device="cuda")
 
         def run():
             counts.zero_()
-            return LD.qc_decode(llr, code, 20, variant, 0.75, early_stop=es, precision="exact", ref_bits=payload,
+            return LD.qc_decode(llr, code, 20, variant, 0.75, early_stop=es, precision=prec, ref_bits=payload,
                                 want_hard=False, want_iters=es, counts=counts)
 
         ms, r = timed(run, a.reps)
-        key = f"{variant}_{'es' if es else 'fixed'}"
+        key = f"{prec}_{variant}_{'es' if es else 'fixed'}"
         res[key] = {"ms": ms, "gbit_s": a.batch * a.k / ms / 1e6, "counts": counts.tolist()}
         if es:
             res[key]["mean_iters"] = float(r["iters"].float().mean())
