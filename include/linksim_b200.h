@@ -80,6 +80,10 @@ int ls_binary_source(uint64_t seed, uint64_t stream_id, int64_t count, uint8_t *
  * groups index `points` (2^m complex64, interleaved, device).  nsym symbols. */
 int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, float *x,
                 void *stream);
+/* The same into complex128 (precision "double", sweep.py:170, 352): points64
+ * are the f64 constellation points. */
+int ls_map_bits64(const uint8_t *bits, int64_t nsym, int m, const double *points64, double *x,
+                  void *stream);
 
 /* awgn(x, no, rng) (channel.py:33-40) for complex64 x: x + sqrt(no/2) * z with
  * z drawn from a counter-based Philox4x32-10 / Box-Muller stream keyed by
@@ -97,6 +101,10 @@ int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t st
 int ls_standard_normal(uint64_t seed, uint64_t stream_id, int64_t count, double *out, void *stream);
 int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
                   float *y, void *stream);
+/* awgn for complex128 x (precision "double"): the same normals, noise kept
+ * in f64 and added in f64 (channel.py:27-40 with dtype complex128). */
+int ls_awgn_numpy64(const double *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
+                    double *y, void *stream);
 
 /* demap_app / demap_maxlog (mapping.py:110-158) for any 2^m points:
  * y complex64 [nsym], scalar no (>0) or per-symbol `no_vec` (nullable),
@@ -106,6 +114,9 @@ int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t seed, uint6
  * non-null, m values per symbol. */
 int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
              const double *points64, int m, int mode, float *llr32, double *llr64, void *stream);
+/* ls_demap / ls_demap_qam on complex128 symbols (precision "double"). */
+int ls_demap64(const double *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+               const double *points64, int m, int mode, float *llr32, double *llr64, void *stream);
 
 /* Same as ls_demap for Gray QAM (mapping.py:33-48), using the product
  * structure: each bit's LLR is a log-sum-exp over the 2^(m/2) levels of its
@@ -114,6 +125,9 @@ int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, cons
 int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec,
                  const double *prior, const double *amp, const int32_t *lab, int m, int mode,
                  float *llr32, double *llr64, void *stream);
+int ls_demap_qam64(const double *y, int64_t nsym, double no, const double *no_vec,
+                   const double *prior, const double *amp, const int32_t *lab, int m, int mode,
+                   float *llr32, double *llr64, void *stream);
 
 /* Fused map_bits -> awgn -> demap_app|maxlog for Gray QAM (sweep.py:352-356
  * in one pass): coded bits [nsym*m] -> f32 LLRs [nsym*m].  The noisy symbols

@@ -35,6 +35,10 @@ _SIGS = {
     "ls_graph_destroy": [_vp],
     "ls_binary_source": [_u64, _u64, _i64, _vp, _vp],
     "ls_map_bits": [_vp, _i64, _int, _vp, _vp, _vp],
+    "ls_map_bits64": [_vp, _i64, _int, _vp, _vp, _vp],
+    "ls_awgn_numpy64": [_vp, _i64, _dbl, _u64, _u64, _vp, _vp],
+    "ls_demap64": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "ls_demap_qam64": [_vp, _i64, _dbl, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_awgn": [_vp, _i64, _dbl, _u64, _u64, _vp, _vp],
     "ls_demap": [_vp, _i64, _dbl, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],
     "ls_demap_qam": [_vp, _i64, _dbl, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp, _vp],

@@ -23,7 +23,9 @@ NOISE_KINDS = ("numpy", "philox")
 
 
 def awgn(x, no: float, rng: RngStream, device: bool = False, offset: int = 0, noise: str = "numpy"):
-    """x + CN(0, no) per element (channel.py:33-40); complex64 arithmetic.
+    """x + CN(0, no) per element (channel.py:33-40) in x's precision: the
+    noise is cast to x.dtype as the reference does, so complex64 input gets
+    complex64 arithmetic and complex128 input (precision "double") f64.
     `offset` (even, philox noise only) = index of x's first element in the
     full stream."""
     if no < 0:
@@ -31,6 +33,15 @@ def awgn(x, no: float, rng: RngStream, device: bool = False, offset: int = 0, no
     if noise not in NOISE_KINDS:
         raise ValueError(f"unknown noise generator {noise!r}")
     was_np = not L.is_tensor(x)
+    c128 = (x.dtype == L.torch().complex128) if L.is_tensor(x) else (np.asarray(x).dtype == np.complex128)
+    if c128:
+        if noise != "numpy" or offset:
+            raise ValueError("awgn: complex128 input takes the numpy-exact noise of the whole array")
+        tx = L.to_device(x, "complex128")
+        out = L.empty(tx.shape, "complex128")
+        L.call("ls_awgn_numpy64", L.ptr(tx), tx.numel(), float(no), rng.seed & _MASK64, rng.stream_id & _MASK64,
+               L.ptr(out), L.stream_ptr())
+        return L.to_host(out) if (was_np and not device) else out
     tx = L.to_device(x, "complex64")
     out = L.empty(tx.shape, "complex64")
     if noise == "numpy":
@@ -52,11 +63,13 @@ def standard_normal(count: int, rng: RngStream, device: bool = False):
     return out if device else L.to_host(out)
 
 
-def complex_gaussian(shape, rng: RngStream, variance: float = 1.0, dtype=np.complex64,
+def complex_gaussian(shape, rng: RngStream, variance: float = 1.0, dtype=np.complex128,
                      device: bool = False, noise: str = "numpy"):
-    """Circularly-symmetric complex Gaussian draws (channel.py:24-30)."""
-    if np.dtype(dtype) != np.complex64:
-        raise ValueError("complex_gaussian: the B200 path produces complex64")
-    zeros = L.zeros(tuple(int(s) for s in np.atleast_1d(shape)), "complex64")
+    """Circularly-symmetric complex Gaussian draws (channel.py:24-30),
+    complex128 by default as in the reference, or complex64."""
+    dt = np.dtype(dtype)
+    if dt not in (np.complex64, np.complex128):
+        raise ValueError("complex_gaussian: dtype must be complex64 or complex128")
+    zeros = L.zeros(tuple(int(s) for s in np.atleast_1d(shape)), str(dt))
     z = awgn(zeros, variance, rng, device=True, noise=noise)
     return z if device else L.to_host(z)

@@ -82,6 +82,18 @@ __global__ void k_map_bits(const uint8_t *__restrict__ bits, int64_t nsym, int m
   }
 }
 
+// complex128 points (precision "double": the reference keeps map_bits' f64
+// points, sweep.py:170, 352)
+__global__ void k_map_bits64(const uint8_t *__restrict__ bits, int64_t nsym, int m,
+                             const double2 *__restrict__ pts, double2 *__restrict__ x) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int lab = 0;
+    for (int t = 0; t < m; ++t) lab = (lab << 1) | (bits[s * m + t] & 1);
+    x[s] = pts[lab];
+  }
+}
+
 // ------------------------------------------------------------ awgn (fast mode)
 // Counter-based: element pair q uses Philox4x32 counter (q, stream lo, stream hi, 0)
 // under key (seed lo, seed hi); Box-Muller gives two complex normals per call.
@@ -226,17 +238,25 @@ __global__ void k_modem_qam(const uint8_t *__restrict__ bits, int64_t nsym, cons
 }
 
 // ------------------------------------------------------------ demapper
+// received symbol s as (re, im) in f64: complex64 input is upcast as numpy
+// does (mapping.py:120), complex128 read as is
+__device__ __forceinline__ double2 ld_sym(const float2 *__restrict__ y, int64_t s) {
+  const float2 v = y[s];
+  return make_double2((double)v.x, (double)v.y);
+}
+__device__ __forceinline__ double2 ld_sym(const double2 *__restrict__ y, int64_t s) { return y[s]; }
+
 // mapping.py:110-143: logits = -|y - p|^2 / no (f64), LLR_j = LSE(bit_j=1) -
 // LSE(bit_j=0) with scipy's max + log1p(sum of the others), or max - max.
-template <int MAXP>
-__global__ void k_demap(const float2 *__restrict__ y, int64_t nsym, double no,
+template <int MAXP, class YT>
+__global__ void k_demap(const YT *__restrict__ y, int64_t nsym, double no,
                         const double *__restrict__ no_vec, const double *__restrict__ prior,
                         const double2 *__restrict__ pts, int m, int mode, float *__restrict__ llr32,
                         double *__restrict__ llr64) {
   const int P = 1 << m;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const float2 ys = y[s];
+    const double2 ys = ld_sym(y, s);
     const double yr = ys.x, yi = ys.y;
     const double nos = no_vec ? no_vec[s] : no;
     double lg[MAXP];
@@ -293,15 +313,15 @@ struct QamAxes {
   int lab[16];      // axis label of each level, MSB first
 };
 
-template <int HALF>
-__global__ void k_demap_qam(const float2 *__restrict__ y, int64_t nsym, double no,
+template <int HALF, class YT>
+__global__ void k_demap_qam(const YT *__restrict__ y, int64_t nsym, double no,
                             const double *__restrict__ no_vec, const double *__restrict__ prior,
                             const QamAxes A, int mode, float *__restrict__ llr32,
                             double *__restrict__ llr64) {
   constexpr int L = 1 << HALF, M = 2 * HALF;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const float2 ys = y[s];
+    const double2 ys = ld_sym(y, s);
     const double inv = 1.0 / (no_vec ? no_vec[s] : no);
     double out[M];
 #pragma unroll
@@ -657,6 +677,15 @@ int ls_map_bits(const uint8_t *bits, int64_t nsym, int m, const float *points, f
   return LS_OK;
 }
 
+int ls_map_bits64(const uint8_t *bits, int64_t nsym, int m, const double *points64, double *x, void *stream) {
+  if (m < 1 || m > 12) return fail(LS_EINVAL, "num_bits_per_symbol must be in [1, 12]");
+  if (!nsym) return LS_OK;
+  k_map_bits64<<<grid_for(nsym, 256), 256, 0, as_stream(stream)>>>(
+      bits, nsym, m, reinterpret_cast<const double2 *>(points64), reinterpret_cast<double2 *>(x));
+  LS_CHECK_LAUNCH("ls_map_bits64");
+  return LS_OK;
+}
+
 int ls_awgn_at(const float *x, int64_t offset, int64_t count, double no, uint64_t seed, uint64_t stream_id,
                float *y, void *stream) {
   if (no < 0) return fail(LS_EINVAL, "noise variance must be >= 0, got " + std::to_string(no));
@@ -678,13 +707,15 @@ int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t st
   return ls_awgn_at(x, 0, count, no, seed, stream_id, y, stream);
 }
 
-int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
-             const double *points64, int m, int mode, float *llr32, double *llr64, void *stream) {
+}  // extern "C"
+
+template <class YT>
+static int demap_any(const YT *yy, int64_t nsym, double no, const double *no_vec, const double *prior,
+                     const double *points64, int m, int mode, float *llr32, double *llr64, void *stream) {
   if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
   if (m < 1 || m > 8) return fail(LS_EINVAL, "demap: num_bits_per_symbol must be in [1, 8]");
   if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
   if (!nsym) return LS_OK;
-  const float2 *yy = reinterpret_cast<const float2 *>(y);
   const double2 *pp = reinterpret_cast<const double2 *>(points64);
   cudaStream_t s = as_stream(stream);
   if (m <= 4)
@@ -697,9 +728,26 @@ int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, cons
   return LS_OK;
 }
 
-int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
-                 const double *amp, const int32_t *lab, int m, int mode, float *llr32, double *llr64,
-                 void *stream) {
+extern "C" {
+
+int ls_demap(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+             const double *points64, int m, int mode, float *llr32, double *llr64, void *stream) {
+  return demap_any(reinterpret_cast<const float2 *>(y), nsym, no, no_vec, prior, points64, m, mode, llr32, llr64,
+                   stream);
+}
+
+int ls_demap64(const double *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+               const double *points64, int m, int mode, float *llr32, double *llr64, void *stream) {
+  return demap_any(reinterpret_cast<const double2 *>(y), nsym, no, no_vec, prior, points64, m, mode, llr32, llr64,
+                   stream);
+}
+
+}  // extern "C"
+
+template <class YT>
+static int demap_qam_any(const YT *yy, int64_t nsym, double no, const double *no_vec, const double *prior,
+                         const double *amp, const int32_t *lab, int m, int mode, float *llr32, double *llr64,
+                         void *stream) {
   if (!no_vec && !(no > 0)) return fail(LS_EINVAL, "demap: noise variance must be > 0");
   if (m < 2 || m > 8 || (m % 2)) return fail(LS_EINVAL, "demap_qam: bits per symbol must be 2, 4, 6 or 8");
   if (mode != LS_DEMAP_APP && mode != LS_DEMAP_MAXLOG) return fail(LS_EINVAL, "demap: unknown mode");
@@ -711,7 +759,6 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, 
     A.amp[l] = l < L ? amp[l] : 0.0;
     A.lab[l] = l < L ? lab[l] : 0;
   }
-  const float2 *yy = reinterpret_cast<const float2 *>(y);
   cudaStream_t s = as_stream(stream);
   const unsigned g = grid_for(nsym, 256);
   switch (m) {
@@ -722,6 +769,22 @@ int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, 
   }
   LS_CHECK_LAUNCH("ls_demap_qam");
   return LS_OK;
+}
+
+extern "C" {
+
+int ls_demap_qam(const float *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+                 const double *amp, const int32_t *lab, int m, int mode, float *llr32, double *llr64,
+                 void *stream) {
+  return demap_qam_any(reinterpret_cast<const float2 *>(y), nsym, no, no_vec, prior, amp, lab, m, mode, llr32,
+                       llr64, stream);
+}
+
+int ls_demap_qam64(const double *y, int64_t nsym, double no, const double *no_vec, const double *prior,
+                   const double *amp, const int32_t *lab, int m, int mode, float *llr32, double *llr64,
+                   void *stream) {
+  return demap_qam_any(reinterpret_cast<const double2 *>(y), nsym, no, no_vec, prior, amp, lab, m, mode, llr32,
+                       llr64, stream);
 }
 
 int ls_modem_qam(const uint8_t *bits, int64_t nsym, int m, const float *points, const double *amp,

@@ -379,6 +379,16 @@ __global__ void k_awgn_apply(const float2 *__restrict__ x, int64_t S, double sca
   }
 }
 
+// complex128 (precision "double", channel.py:27-40): noise (sqrt(no/2) * z)
+// stays f64 and is added in f64
+__global__ void k_awgn_apply64(const double2 *__restrict__ x, int64_t S, double scale, const double *__restrict__ z,
+                               double2 *__restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S; e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = x[e];
+    y[e] = make_double2(a.x + scale * z[e], a.y + scale * z[S + e]);
+  }
+}
+
 static int normals(uint64_t seed, uint64_t sid, int64_t count, double *out, cudaStream_t s) {
   retain_pool_memory();
   const int64_t words = (int64_t)((double)count * 1.06) + 8 * kZG;
@@ -453,6 +463,29 @@ extern "C" int ls_awgn_numpy(const float *x, int64_t count, double no, uint64_t 
                                                       reinterpret_cast<float2 *>(y));
     e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_status(e, "ls_awgn_numpy");
+  }
+  cudaFreeAsync(z, s);
+  return rc;
+}
+
+extern "C" int ls_awgn_numpy64(const double *x, int64_t count, double no, uint64_t seed, uint64_t stream_id,
+                               double *y, void *stream) {
+  if (no < 0) return fail(LS_EINVAL, "noise variance must be >= 0, got " + std::to_string(no));
+  if (!count) return LS_OK;
+  cudaStream_t s = as_stream(stream);
+  if (no == 0) {
+    cudaError_t e = cudaMemcpyAsync(y, x, (size_t)count * 16, cudaMemcpyDeviceToDevice, s);
+    return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_awgn_numpy64");
+  }
+  double *z = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&z, sizeof(double) * 2 * count, s);
+  if (e != cudaSuccess) return cuda_status(e, "ls_awgn_numpy64(workspace)");
+  int rc = normals(seed, stream_id, 2 * count, z, s);
+  if (rc == LS_OK) {
+    k_awgn_apply64<<<grid_for(count, 256), 256, 0, s>>>(reinterpret_cast<const double2 *>(x), count,
+                                                        sqrt(no / 2.0), z, reinterpret_cast<double2 *>(y));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_status(e, "ls_awgn_numpy64");
   }
   cudaFreeAsync(z, s);
   return rc;

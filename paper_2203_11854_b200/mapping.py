@@ -120,26 +120,34 @@ class Constellation:
         return self._dev[dtype]
 
 
-def map_bits(bits, constellation: Constellation, device: bool = False):
+def map_bits(bits, constellation: Constellation, device: bool = False, dtype: str = "complex64"):
     """Big-endian m-bit groups -> points (mapping.py:96-107).
 
-    Output is complex64 (the sweep engine's `astype(complex64)`,
-    sweep.py:352, is folded in); numpy in -> numpy out unless device=True.
+    dtype "complex64" folds in the sweep engine's `astype(complex64)`
+    (sweep.py:352, precision "single"); "complex128" keeps the f64 points
+    (precision "double").  numpy in -> numpy out unless device=True.
     """
+    if dtype not in ("complex64", "complex128"):
+        raise ValueError(f"map_bits: unsupported dtype {dtype!r}")
     was_np = not L.is_tensor(bits)
     m = constellation.num_bits_per_symbol
     tb = L.to_device(bits, "uint8")
     if tb.shape[-1] % m != 0:
         raise ValueError(f"bit count {tb.shape[-1]} not divisible by {m} bits/symbol")
-    out = L.empty(tuple(tb.shape[:-1]) + (tb.shape[-1] // m,), "complex64")
-    L.call("ls_map_bits", L.ptr(tb), out.numel(), m, L.ptr(constellation.device_points("float32")),
-           L.ptr(out), L.stream_ptr())
+    out = L.empty(tuple(tb.shape[:-1]) + (tb.shape[-1] // m,), dtype)
+    if dtype == "complex64":
+        L.call("ls_map_bits", L.ptr(tb), out.numel(), m, L.ptr(constellation.device_points("float32")),
+               L.ptr(out), L.stream_ptr())
+    else:
+        L.call("ls_map_bits64", L.ptr(tb), out.numel(), m, L.ptr(constellation.device_points("float64")),
+               L.ptr(out), L.stream_ptr())
     return L.to_host(out) if (was_np and not device) else out
 
 
 def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str, device: bool):
     was_np = not L.is_tensor(y)
-    ty = L.to_device(y, "complex64")
+    c128 = (y.dtype == L.torch().complex128) if L.is_tensor(y) else (np.asarray(y).dtype == np.complex128)
+    ty = L.to_device(y, "complex128" if c128 else "complex64")
     m = constellation.num_bits_per_symbol
     tp = None
     if prior is not None:
@@ -168,11 +176,12 @@ def _demap(y, no, constellation: Constellation, prior, mode: int, out_dtype: str
     axes = constellation.qam_axes()
     if axes is not None:
         amp, lab = axes
-        L.call("ls_demap_qam", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), L.ptr(tp), amp.ctypes.data,
+        L.call("ls_demap_qam64" if c128 else "ls_demap_qam", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec),
+               L.ptr(tp), amp.ctypes.data,
                lab.ctypes.data, m, mode, None if is64 else L.ptr(out), L.ptr(out) if is64 else None,
                L.stream_ptr())
         return L.to_host(out) if (was_np and not device) else out
-    L.call("ls_demap", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), L.ptr(tp),
+    L.call("ls_demap64" if c128 else "ls_demap", L.ptr(ty), ty.numel(), no_s, L.ptr(no_vec), L.ptr(tp),
            L.ptr(constellation.device_points("float64")), m, mode,
            None if is64 else L.ptr(out), L.ptr(out) if is64 else None, L.stream_ptr())
     return L.to_host(out) if (was_np and not device) else out

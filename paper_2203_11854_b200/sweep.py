@@ -180,9 +180,12 @@ class Pipeline:
             if self.decoder_mode not in ("exact", "fast"):
                 raise ConfigError("code.decoder.mode", f"unknown mode {self.decoder_mode!r}")
             self.decoder_precision = dec.get("precision", "auto")
-            if self.decoder_precision not in ("auto", "fp32", "fp16x2"):
+            if self.decoder_precision not in ("auto", "fp32", "fp16x2", "fp32-full"):
                 raise ConfigError("code.decoder.precision",
                                   f"unknown precision {self.decoder_precision!r}")
+            if cfg.precision == "double" and self.decoder_mode != "exact":
+                raise ConfigError("precision", "'double' runs the exact f64 chain; decoder.mode 'fast' "
+                                               "computes in f32 / fp16")
             self.payload_bits = code["k"]
             self.coded_bits = code["n"]
             self.coderate = code["k"] / code["n"]
@@ -208,7 +211,7 @@ class Pipeline:
     def fused_modem(self) -> bool:
         """Fast chain: one fused map+AWGN+demap pass for Gray QAM."""
         return (self.family != "none" and self.decoder_mode == "fast" and self.noise == "philox"
-                and self.constellation.qam_axes() is not None)
+                and self.cfg.precision == "single" and self.constellation.qam_axes() is not None)
 
     def _llr(self, ebno_db: float, batch_size: int, rng: RngStream, lo: int = 0):
         """Payload and f32 LLRs of rows [lo, lo + batch_size) of a batch: the
@@ -222,15 +225,17 @@ class Pipeline:
         if self.fused_modem:
             llr = modem_qam(coded, self.constellation, no, rng.child(2), self.demapper, offset=sym0)
             return payload, llr
-        x = map_bits(coded, self.constellation, device=True)
+        double = self.cfg.precision == "double"  # complex128 symbols, f64 LLRs (sweep.py:170, 352, 362)
+        x = map_bits(coded, self.constellation, device=True, dtype="complex128" if double else "complex64")
         y = awgn(x, no, rng.child(2), device=True, offset=sym0, noise=self.noise)
-        llr = self.demap(y, no, self.constellation, out_dtype="float32", device=True)
+        llr = self.demap(y, no, self.constellation, out_dtype="float64" if double else "float32", device=True)
         return payload, llr
 
     @property
     def qc_exact(self) -> bool:
-        """Exact mode served by the on-chip QC decoder (min-sum variants)."""
-        if self.family == "none" or self.decoder_mode != "exact":
+        """Exact mode served by the on-chip QC decoder (min-sum variants on
+        f32 LLRs; precision 'double' decodes f64 LLRs on the CSR engine)."""
+        if self.family == "none" or self.decoder_mode != "exact" or self.cfg.precision == "double":
             return False
         if getattr(self, "_qc_exact", None) is None:
             self._qc_exact = qc_has_kernel(self.ldpc, precision="exact", variant=self.bp_variant)

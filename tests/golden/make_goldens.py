@@ -124,6 +124,37 @@ def chain_fixture(core, ldpc, mapping, channel, k, n, m, ebno_db, batch, seed, s
     return out
 
 
+def chain_double_fixture(core, ldpc, mapping, channel, k, n, m, ebno_db, batch, seed, sid, variants):
+    """Pipeline.run_batch with precision 'double' (sweep.py:170, 352, 362):
+    complex128 symbols and noise, f64 demapper output decoded as f64.  Done by
+    hand to keep the intermediates, then checked against the reference's own
+    Pipeline.run_batch."""
+    import linksim.sweep as sweep
+
+    code = ldpc.LdpcCode5G(k, n)
+    const = mapping.Constellation("qam", m)
+    rng = core.RngStream(seed, sid)
+    no = core.ebnodb2no(ebno_db, m, k / n)
+    payload = core.binary_source([batch, k], rng.child(0))
+    coded = ldpc.ldpc5g_encode(payload, code)
+    x = mapping.map_bits(coded, const).astype(np.complex128)
+    y = channel.awgn(x, no, rng.child(2))
+    llr = np.asarray(mapping.demap_app(y, no, const), dtype=np.float64)
+    out = dict(payload=np.packbits(payload, axis=-1), y=y, llr=llr, no=np.float64(no),
+               dims=np.array([k, n, m, batch, code.base_graph, code.z], np.int64))
+    for var in variants:
+        tag = var.replace("-", "_")
+        dec = ldpc.ldpc5g_decode(llr, code, num_iter=20, variant=var)
+        out[f"{tag}_decoded"] = np.packbits(dec, axis=-1)
+        cfg = sweep.SimConfig.from_dict({
+            "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"variant": var, "num_iter": 20}},
+            "modulation": {"kind": "qam", "bits_per_symbol": m},
+            "sweep": {"ebno_db": [ebno_db], "batch_size": batch}, "seed": seed, "precision": "double"})
+        p2, d2 = sweep.Pipeline(cfg).run_batch(ebno_db, batch, core.RngStream(seed, sid))
+        assert np.array_equal(p2, payload) and np.array_equal(d2, dec), "by-hand chain != reference Pipeline"
+    return out
+
+
 def encoder_fixture(core, ldpc):
     out = {}
     for i, (k, n) in enumerate([(256, 512), (8448, 16896), (4096, 8192), (4096, 12288),
@@ -193,6 +224,12 @@ def hamming_fixture(core, ldpc, ParityCheckMatrix):
 def main():
     core, ldpc, mapping, channel, ParityCheckMatrix = _ref()
     meta = _meta()
+    # config 1 in precision 'double' (complex128 / f64 chain)
+    np.savez_compressed(os.path.join(OUT, "chain_c1_double.npz"), meta=meta,
+                        **chain_double_fixture(core, ldpc, mapping, channel, 256, 512, 2, 2.0, 48, 42,
+                                               (1 << 32) | 1, ("min-sum", "scaled-min-sum", "sum-product")))
+    if "--double-only" in sys.argv:
+        return
     np.savez_compressed(os.path.join(OUT, "base_graphs.npz"), meta=meta, **base_graphs(ldpc))
     np.savez_compressed(os.path.join(OUT, "rng.npz"), meta=meta, **rng_fixture(core, channel))
     np.savez_compressed(os.path.join(OUT, "encoder.npz"), meta=meta, **encoder_fixture(core, ldpc))

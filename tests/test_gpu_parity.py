@@ -622,7 +622,7 @@ def test_awgn_numpy_noise_bit_exact(golden):
     z = golden("rng")
     for i in range(3):
         seed, sid = (int(x) for x in z[f"key{i}"])
-        cg = lb.complex_gaussian([4, 500], lb.RngStream(seed, sid).child(2), variance=0.3)
+        cg = lb.complex_gaussian([4, 500], lb.RngStream(seed, sid).child(2), variance=0.3, dtype=np.complex64)
         assert np.array_equal(cg, z[f"cn{i}"])
 
 
@@ -747,3 +747,34 @@ def test_run_sweep_worker_count_invariance():
     assert any(p[5] == "target-errors" for p in base)
     for w in (3, 8):
         assert key(lb.run_sweep(cfg, num_workers=w)) == base, w
+
+
+@pytest.mark.parametrize("variant", ["min-sum", "scaled-min-sum", "sum-product"])
+def test_pipeline_double_precision_chain(golden, variant):
+    """precision 'double' (sweep.py:170, 352, 362): complex128 symbols and
+    numpy-exact complex128 noise, f64 demapper LLRs decoded in f64 -- equal to
+    the reference's double-precision run_batch (golden chain_c1_double)."""
+    d = golden("chain_c1_double")
+    k, n, m, B, _, _ = (int(x) for x in d["dims"])
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"variant": variant}},
+        "modulation": {"kind": "qam", "bits_per_symbol": m},
+        "sweep": {"ebno_db": [2.0], "batch_size": B}, "seed": 42, "precision": "double"})
+    pipe = lb.Pipeline(cfg)
+    rng = lb.RngStream(42, (1 << 32) | 1)
+    payload, llr = pipe._llr(2.0, B, rng)
+    assert llr.dtype == torch.float64
+    lr = d["llr"]
+    assert np.allclose(llr.cpu().numpy(), lr, rtol=1e-9, atol=1e-9)
+    payload, dec = pipe.run_batch(2.0, B, rng)
+    assert np.array_equal(np.packbits(payload, axis=-1), d["payload"])
+    assert np.array_equal(np.packbits(dec, axis=-1), d[f"{variant.replace('-', '_')}_decoded"])
+    # the symbols: complex128 map + numpy-exact complex128 noise, bit for bit
+    x = lb.map_bits(lb.ldpc5g_encode(payload, pipe.ldpc), pipe.constellation, dtype="complex128")
+    y = lb.awgn(x, float(d["no"]), rng.child(2))
+    assert y.dtype == np.complex128 and np.array_equal(y, d["y"])
+    with pytest.raises(lb.ConfigError):
+        lb.Pipeline(lb.SimConfig.from_dict({
+            "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"mode": "fast"}},
+            "modulation": {"kind": "qam", "bits_per_symbol": m}, "precision": "double",
+            "sweep": {"ebno_db": [2.0], "batch_size": B}}))
