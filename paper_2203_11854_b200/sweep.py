@@ -360,8 +360,11 @@ def sweep_points(cfg: SimConfig, payload_bits: int, eval_batch, dist=None, batch
                 if i % world == rank:
                     eval_batch(snr_idx, ebno_db, bidx, local[i // world])
             if dist:
-                gathered = [torch.zeros_like(local) for _ in range(world)]
-                dist.all_gather(gathered, local)
+                # NCCL gathers the device counters in place; gloo (CPU test
+                # groups, or ranks sharing one GPU) needs host tensors
+                src = local if dist.get_backend() == "nccl" else local.cpu()
+                gathered = [torch.zeros_like(src) for _ in range(world)]
+                dist.all_gather(gathered, src)
                 allc = torch.stack(gathered).cpu()  # [world, per, 2]
             else:
                 allc = local.cpu().unsqueeze(0)

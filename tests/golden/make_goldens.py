@@ -155,6 +155,32 @@ def chain_double_fixture(core, ldpc, mapping, channel, k, n, m, ebno_db, batch, 
     return out
 
 
+SWEEP_C1 = {"code": {"family": "ldpc5g", "k": 256, "n": 512,
+                     "decoder": {"variant": "min-sum", "num_iter": 20}},
+            "modulation": {"kind": "qam", "bits_per_symbol": 2},
+            "sweep": {"ebno_db": [1.0, 2.0, 3.0, 4.0, 5.0, 6.0], "batch_size": 64,
+                      "target_block_errors": 12, "max_batches_per_point": 5},
+            "seed": 11}
+
+
+def sweep_fixture():
+    """The reference's own run_sweep (sweep.py:411-476) on a small config-1
+    sweep: per-point counts, batches and stop reasons (deterministic in
+    (config, seed) for any worker count), plus its CSV."""
+    import linksim.sweep as sweep
+
+    res = sweep.run_sweep(sweep.SimConfig.from_dict(SWEEP_C1), num_workers=4)
+    pts = res.points
+    csv_text = sweep.format_csv(res)
+    return dict(config=json.dumps(SWEEP_C1),
+                ebno=np.array([p.ebno_db for p in pts]), bits=np.array([p.bits for p in pts]),
+                bit_errors=np.array([p.bit_errors for p in pts]), blocks=np.array([p.blocks for p in pts]),
+                block_errors=np.array([p.block_errors for p in pts]),
+                batches=np.array([p.batches for p in pts]),
+                stop_reason=np.array([p.stop_reason for p in pts]),
+                csv_header=csv_text.splitlines()[0])
+
+
 def encoder_fixture(core, ldpc):
     out = {}
     for i, (k, n) in enumerate([(256, 512), (8448, 16896), (4096, 8192), (4096, 12288),
@@ -228,7 +254,8 @@ def main():
     np.savez_compressed(os.path.join(OUT, "chain_c1_double.npz"), meta=meta,
                         **chain_double_fixture(core, ldpc, mapping, channel, 256, 512, 2, 2.0, 48, 42,
                                                (1 << 32) | 1, ("min-sum", "scaled-min-sum", "sum-product")))
-    if "--double-only" in sys.argv:
+    np.savez_compressed(os.path.join(OUT, "sweep_c1.npz"), meta=meta, **sweep_fixture())
+    if "--new-only" in sys.argv:
         return
     np.savez_compressed(os.path.join(OUT, "base_graphs.npz"), meta=meta, **base_graphs(ldpc))
     np.savez_compressed(os.path.join(OUT, "rng.npz"), meta=meta, **rng_fixture(core, channel))
