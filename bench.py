@@ -227,8 +227,7 @@ def run_b200(a, rank, world, local_rank):
     # BP decoder (bit-identical to ldpc.py:86-172) over the whole mother graph
     cfg = lb.SimConfig.from_dict({
         "code": {"family": "ldpc5g", "k": K_INFO, "n": N_TX,
-                 "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "exact",
-                             "early_stop": bool(a.early_stop)}},
+                 "decoder": {"variant": a.variant, "num_iter": a.iters, "mode": "exact"}},
         "modulation": {"kind": "qam", "bits_per_symbol": M_BITS},
         "sweep": {"ebno_db": [a.ebno], "batch_size": a.batch}, "seed": a.seed})
     pipe = lb.Pipeline(cfg)
@@ -496,7 +495,8 @@ def e2e_chain(a, pipe, rank, world, dist, steps=3):
     el = _wall_max(dist, time.perf_counter() - t)
     return {"value": world * B * K_INFO * steps / el / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": 0,
             "d2h_bytes_per_step": 2 * B * K_INFO,
-            "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys"}
+            "api": "Pipeline.run_batch -> numpy (payload, decoded); inputs are the RngStream keys; the "
+                   "reference's Pipeline semantics, i.e. the decoder's early stop is on (sweep.py:335-336)"}
 
 
 def e2e_decode(a, pipe, rank, world, dist, steps=3):

@@ -87,8 +87,8 @@ int ls_map_bits64(const uint8_t *bits, int64_t nsym, int m, const double *points
 
 /* awgn(x, no, rng) (channel.py:33-40) for complex64 x: x + sqrt(no/2) * z with
  * z drawn from a counter-based Philox4x32-10 / Box-Muller stream keyed by
- * (seed, stream_id).  Statistically equivalent to the reference; the
- * bit-exact numpy-ziggurat replica is SURVEY.md 8f item 2. */
+ * (seed, stream_id).  Statistically equivalent to the reference (fast
+ * mode); ls_awgn_numpy below is the bit-exact numpy-ziggurat replica. */
 int ls_awgn(const float *x, int64_t count, double no, uint64_t seed, uint64_t stream_id, float *y,
             void *stream);
 
@@ -172,7 +172,10 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
 
 /* ldpc5g_decode (ldpc.py:354-365) FAST mode on the QC structure, fused with
  * derate_match, hard decision (core.py:102-104) and count_errors
- * (core.py:93-99): one CTA per codeword, messages on chip.  llr [B,n] f32
+ * (core.py:93-99), messages on chip.  The fp16x2 kernels run a pair of
+ * codewords per CTA (persistent CTAs, one or two slots per SM); the exact /
+ * fp32 full-graph kernel (LS_QC_EXACT / LS_QC_FULL32) one codeword per
+ * persistent CTA.  llr [B,n] f32
  * rate-matched.  Outputs (all nullable): hard_k [B,k] info bits,
  * llr_out [B,n_full] f32 mother LLRs (ln p1/p0), iters_used [B],
  * counts[2] += (bit errors, block errors) against ref_bits [B,k].
@@ -207,6 +210,15 @@ int ls_qc_live_rows(const ls_code *code);
 /* 1 if a compile-time specialised kernel serves this code with these flags
  * (LS_QC_PRUNE / LS_QC_FP16), else 0 (fp32 falls back to the runtime-Z kernel). */
 int ls_qc_has_kernel(const ls_code *code, int flags);
+
+/* hard_decide(llr) (core.py:102-104): out[i] = llr[i] > 0, f32 or f64. */
+int ls_hard_decide(const void *llr, int is_f64, int64_t count, uint8_t *out, void *stream);
+
+/* exit_mutual_information(llr, bits) (ldpc.py:175-188): writes
+ * clip(1 - mean(log2(1 + exp(clip(-(2b-1) L, +-40)))), 0, 1) to *out
+ * (device f64); bits as f64 {0, 1}.  Deterministic reduction order. */
+int ls_exit_mutual_information(const double *llr, const double *bits, int64_t count, double *out,
+                               void *stream);
 
 /* count_errors(b, b_hat) (core.py:93-99): counts[2] += (bit, block) errors. */
 int ls_count_errors(const uint8_t *b, const uint8_t *b_hat, int64_t batch, int64_t len,

@@ -16,8 +16,9 @@ see tests/test_oracle_golden.py).  Where the reference's arithmetic lives in
 third-party code the restatement names it:
   * numpy 2.3.5 Philox4x64-10 / bounded uint8 draw -> oracle/c/oracle.c
   * numpy 2.3.5 Generator.standard_normal (256-level ziggurat) -> called
-    through numpy itself here (same pinned version on the GPU box image); the
-    bit-exact restatement is SURVEY.md A3 and is on the 'next' list.
+    through numpy itself here (same pinned version on the GPU box image) and
+    restated bit-exactly in C (oracle/c/oracle.c, orc_standard_normal;
+    SURVEY.md A3), both pinned to the reference's draws in tests/golden/rng.npz.
   * scipy 1.18.1 special.logsumexp -> restated in `_lse` below.
 """
 from __future__ import annotations
@@ -89,6 +90,24 @@ def standard_normal_pair(shape, seed: int, stream_id: int):
     re = g.standard_normal(shape)
     im = g.standard_normal(shape)
     return re, im
+
+
+def hard_decide(llr):
+    """core.py:102-104: 1 iff L > 0."""
+    return (np.asarray(llr) > 0).astype(np.uint8)
+
+
+def exit_mutual_information(llr, bits) -> float:
+    """ldpc.py:175-188 restated: 1 - mean(log2(1 + exp(clip(-(2b-1)L, +-40)))),
+    clipped to [0, 1]."""
+    llr = np.asarray(llr, dtype=np.float64)
+    bits = np.asarray(bits)
+    if llr.size == 0:
+        raise ValueError("exit_mutual_information: empty input")
+    if llr.shape != bits.shape:
+        raise ValueError("exit_mutual_information: shape mismatch")
+    x = np.clip(-(2.0 * bits - 1.0) * llr, -LLR_MAX, LLR_MAX)
+    return float(np.clip(1.0 - np.mean(np.log2(1.0 + np.exp(x))), 0.0, 1.0))
 
 
 def ebnodb2no(ebno_db: float, m: int, coderate: float) -> float:

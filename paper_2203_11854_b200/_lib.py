@@ -55,6 +55,8 @@ _SIGS = {
     "ls_qc_live_rows": [_vp],
     "ls_qc_has_kernel": [_vp, _int],
     "ls_count_errors": [_vp, _vp, _i64, _i64, _vp, _vp],
+    "ls_hard_decide": [_vp, _int, _i64, _vp, _vp],
+    "ls_exit_mutual_information": [_vp, _vp, _i64, _vp, _vp],
 }
 
 

@@ -6,8 +6,8 @@ fixed seed by its asset tool (/root/reference/pkg/tools/generate_assets.py:
 data/ldpc_bg{1,2}.txt (ldpc.py:191-211).  Parity needs the identical graphs,
 so this module re-derives them with the same published construction and the
 same numpy PCG64 draw sequence instead of shipping the reference's files.
-tests/test_basegraph.py checks the result against the golden copy of the
-reference tables entry by entry.
+tests/test_host.py (test_base_graph_restatement_matches_reference_tables) checks the
+result against the golden copy of the reference tables entry by entry.
 
 Construction (per graph):
   1. accumulate core on parity columns k_b..k_b+3 -- the sum of the four core

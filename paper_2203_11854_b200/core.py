@@ -112,8 +112,13 @@ def compute_bler(b, b_hat) -> float:
 
 
 def hard_decide(llr):
-    """1 iff L > 0 (core.py:102-104)."""
+    """1 iff L > 0 (core.py:102-104): ties and -0.0 decide 0 (k_hard)."""
     was_np = not L.is_tensor(llr)
+    torch = L.torch()
     t = L.to_device(llr)
-    out = (t > 0).to(L.torch().uint8)
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    t = t.contiguous()
+    out = L.empty(tuple(t.shape), "uint8")
+    L.call("ls_hard_decide", L.ptr(t), int(t.dtype == torch.float64), t.numel(), L.ptr(out), L.stream_ptr())
     return L.to_host(out) if was_np else out

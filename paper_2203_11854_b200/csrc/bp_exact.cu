@@ -24,6 +24,8 @@
 
 namespace lsb {
 
+// nodes up to this degree keep their edge values in registers / local
+// memory; higher degrees stream over their edges twice (same results)
 constexpr int kExactMaxDeg = 64;
 
 template <typename T>
@@ -48,6 +50,78 @@ __device__ __forceinline__ T pairwise(const T *x, int n) {
 template <typename T>
 __device__ __forceinline__ T segsum(const T *x, int n) {
   return n == 1 ? x[0] : x[0] + pairwise(x + 1, n - 1);
+}
+
+// numpy pairwise_sum of term(off..off+n-1), n <= 128, without storing the terms
+template <typename T, class F>
+__device__ T pairwise_block(int off, int n, const F &term) {
+  if (n < 8) {
+    T r = (T)-0.0;
+    for (int i = 0; i < n; ++i) r = r + term(off + i);
+    return r;
+  }
+  T r0 = term(off), r1 = term(off + 1), r2 = term(off + 2), r3 = term(off + 3), r4 = term(off + 4),
+    r5 = term(off + 5), r6 = term(off + 6), r7 = term(off + 7);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = r0 + term(off + i); r1 = r1 + term(off + i + 1); r2 = r2 + term(off + i + 2); r3 = r3 + term(off + i + 3);
+    r4 = r4 + term(off + i + 4); r5 = r5 + term(off + i + 5); r6 = r6 + term(off + i + 6); r7 = r7 + term(off + i + 7);
+  }
+  T res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res = res + term(off + i);
+  return res;
+}
+
+// any n: above 128 terms numpy splits the block in two halves (n/2 rounded
+// down to a multiple of 8) and recurses; the recursion is walked here with
+// an explicit stack (device recursion would overflow the thread stack)
+template <typename T, class F>
+__device__ T pairwise_stream(int off, int n, const F &term) {
+  if (n <= 128) return pairwise_block<T>(off, n, term);
+  struct Frame {
+    int off, n, n2, state;
+    T left;
+  };
+  Frame st[24];  // depth log2(n / 128) + 1
+  int sp = 0;
+  st[0] = Frame{off, n, 0, 0, (T)0};
+  T ret = (T)0;
+  bool have = false;  // `ret` holds the value of the frame just finished
+  while (sp >= 0) {
+    Frame &f = st[sp];
+    if (have) {
+      if (f.state == 1) {  // left half done: evaluate the right half
+        f.left = ret;
+        f.state = 2;
+        have = false;
+        st[sp + 1] = Frame{f.off + f.n2, f.n - f.n2, 0, 0, (T)0};
+        ++sp;
+      } else {  // both halves done
+        ret = f.left + ret;
+        --sp;
+      }
+      continue;
+    }
+    if (f.n <= 128) {
+      ret = pairwise_block<T>(f.off, f.n, term);
+      have = true;
+      --sp;
+      continue;
+    }
+    int n2 = f.n / 2;
+    n2 -= n2 % 8;
+    f.n2 = n2;
+    f.state = 1;
+    st[sp + 1] = Frame{f.off, n2, 0, 0, (T)0};
+    ++sp;
+  }
+  return ret;
+}
+
+// x0 + pairwise(x1..x_{n-1}) (numpy add.reduceat of one segment)
+template <typename T, class F>
+__device__ T segsum_stream(int n, const F &term) {
+  return n == 1 ? term(0) : term(0) + pairwise_stream<T>(1, n - 1, term);
 }
 
 __device__ __forceinline__ double phi_d(double x) {
@@ -111,6 +185,61 @@ __global__ void k_ex_check(const int32_t *__restrict__ cptr, const int32_t *__re
   double v2c[kExactMaxDeg];
   for (int64_t c = blockIdx.y; c < m; c += gridDim.y) {
     const int e0 = cptr[c], d = cptr[c + 1] - e0;
+    if (d > kExactMaxDeg) {
+      // high-degree check: the same arithmetic in two streaming passes over
+      // the edges (each v2c recomputed from total and the not yet
+      // overwritten c2v of its own edge), no per-check array
+      auto v2c_at = [&](int j) -> double {
+        const int64_t e = e0 + j;
+        return (double)total[(int64_t)cvar[e] * B + b] - c2v[e * B + b];
+      };
+      int par = 0;
+      for (int j = 0; j < d; ++j) par ^= signbit(v2c_at(j)) ? 1 : 0;
+      if (VARIANT == LS_SUM_PRODUCT) {
+        if (first_f32) {
+          auto pmf = [&](int j) -> float { return phi_f(fabsf((float)v2c_at(j))); };
+          const float ps = segsum_stream<float>(d, pmf);
+          for (int j = 0; j < d; ++j) {
+            const double x = v2c_at(j);
+            float me = phi_f(fmaxf(ps - phi_f(fabsf((float)x)), 1e-12f));
+            me = fminf(fmaxf(me, 0.0f), 30.0f);
+            const int neg = par ^ (signbit(x) ? 1 : 0);
+            c2v[(e0 + j) * B + b] = (neg ? -1.0 : 1.0) * (double)me;
+          }
+        } else {
+          auto pmd = [&](int j) -> double { return phi_d(fabs(v2c_at(j))); };
+          const double ps = segsum_stream<double>(d, pmd);
+          for (int j = 0; j < d; ++j) {
+            const double x = v2c_at(j);
+            double me = phi_d(fmax(ps - phi_d(fabs(x)), 1e-12));
+            me = fmin(fmax(me, 0.0), 30.0);
+            const int neg = par ^ (signbit(x) ? 1 : 0);
+            c2v[(e0 + j) * B + b] = (neg ? -1.0 : 1.0) * me;
+          }
+        }
+      } else {
+        // multiset minimum pair + first argmin == _segment_min2's rule
+        // (ldpc.py:65-74): a tie makes the runner-up equal to min1
+        double mn1 = INFINITY, mn2 = INFINITY;
+        int arg = 0;
+        for (int j = 0; j < d; ++j) {
+          const double a = fabs(v2c_at(j));
+          if (a < mn1) {
+            mn2 = mn1;
+            mn1 = a;
+            arg = j;
+          } else if (a < mn2) {
+            mn2 = a;
+          }
+        }
+        for (int j = 0; j < d; ++j) {
+          const double x = v2c_at(j);
+          const int neg = par ^ (signbit(x) ? 1 : 0);
+          c2v[(e0 + j) * B + b] = __dmul_rn(neg ? -alpha : alpha, j == arg ? mn2 : mn1);
+        }
+      }
+      continue;
+    }
     int par = 0;
     for (int j = 0; j < d; ++j) {
       const int64_t e = e0 + j;
@@ -175,8 +304,13 @@ __global__ void k_ex_var(const int32_t *__restrict__ vptr, const int32_t *__rest
       total[o] = chan[o];
       continue;
     }
-    for (int j = 0; j < d; ++j) x[j] = c2v[(int64_t)vedge[p0 + j] * B + b];
-    const double s = segsum(x, d);
+    double s;
+    if (d > kExactMaxDeg) {
+      s = segsum_stream<double>(d, [&](int j) -> double { return c2v[(int64_t)vedge[p0 + j] * B + b]; });
+    } else {
+      for (int j = 0; j < d; ++j) x[j] = c2v[(int64_t)vedge[p0 + j] * B + b];
+      s = segsum(x, d);
+    }
     T t = (T)((double)chan[o] + s);
     t = t < (T)-40.0 ? (T)-40.0 : (t > (T)40.0 ? (T)40.0 : t);
     total[o] = t;
@@ -305,8 +439,6 @@ int ls_graph_create(int64_t n, int64_t m, const int64_t *cptr, const int64_t *cv
     std::vector<int32_t> fill(vp.begin(), vp.end() - 1);
     for (int64_t e = 0; e < E; ++e) ve[fill[hv[e]]++] = (int32_t)e;  // ascending check order
   }
-  if (max_c > kExactMaxDeg || max_v > kExactMaxDeg)
-    return fail(LS_EINVAL, "node degree above " + std::to_string(kExactMaxDeg) + " is not supported");
   ls_graph *g = new ls_graph();
   g->n = n; g->m = m; g->E = E; g->max_cdeg = max_c; g->max_vdeg = max_v;
   cudaError_t e = cudaSuccess;

@@ -590,6 +590,52 @@ __global__ void k_count(const uint8_t *__restrict__ a, const uint8_t *__restrict
   }
 }
 
+// ------------------------------------------------------------ hard_decide
+// core.py:102-104: 1 iff L > 0 (ties and -0.0 decide 0), f32 or f64 input
+template <typename T>
+__global__ void k_hard(const T *__restrict__ llr, int64_t count, uint8_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = llr[i] > (T)0;
+}
+
+// ------------------------------------------------------------ EXIT mutual information
+// ldpc.py:175-188: I = 1 - mean(log2(1 + exp(clip(-(2b-1) L, +-40)))), f64.
+// Deterministic two-pass sum: fixed per-block partials, then one block.
+constexpr int kMiBlocks = 1184, kMiThreads = 256;
+__global__ void k_mi_partial(const double *__restrict__ llr, const double *__restrict__ bits, int64_t count,
+                             double *__restrict__ part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double x = -(2.0 * bits[i] - 1.0) * llr[i];
+    x = x < -40.0 ? -40.0 : (x > 40.0 ? 40.0 : x);
+    acc += log2(1.0 + exp(x));
+  }
+  __shared__ double red[kMiThreads];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kMiThreads / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_mi_final(const double *__restrict__ part, int n, int64_t count, double *__restrict__ out) {
+  __shared__ double red[kMiThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kMiThreads / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double info = 1.0 - red[0] / (double)count;
+    *out = info < 0.0 ? 0.0 : (info > 1.0 ? 1.0 : info);
+  }
+}
+
 }  // namespace lsb
 
 using namespace lsb;
@@ -855,6 +901,32 @@ int ls_derate(const ls_code *code, const void *llr, int is_f64, int64_t batch, v
     k_derate<float><<<grid_for(total, 256), 256, 0, s>>>(code->p, (const float *)llr, batch, (float *)mother);
   LS_CHECK_LAUNCH("ls_derate");
   return LS_OK;
+}
+
+int ls_hard_decide(const void *llr, int is_f64, int64_t count, uint8_t *out, void *stream) {
+  if (count < 0 || (count && (!llr || !out))) return fail(LS_EINVAL, "hard_decide: bad arguments");
+  if (!count) return LS_OK;
+  cudaStream_t s = as_stream(stream);
+  if (is_f64)
+    k_hard<double><<<grid_for(count, 256), 256, 0, s>>>((const double *)llr, count, out);
+  else
+    k_hard<float><<<grid_for(count, 256), 256, 0, s>>>((const float *)llr, count, out);
+  LS_CHECK_LAUNCH("ls_hard_decide");
+  return LS_OK;
+}
+
+int ls_exit_mutual_information(const double *llr, const double *bits, int64_t count, double *out, void *stream) {
+  if (count <= 0) return fail(LS_EINVAL, "exit_mutual_information: empty input");
+  if (!llr || !bits || !out) return fail(LS_EINVAL, "exit_mutual_information: null argument");
+  cudaStream_t s = as_stream(stream);
+  double *part = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&part, sizeof(double) * kMiBlocks, s);
+  if (e != cudaSuccess) return cuda_status(e, "exit_mutual_information(workspace)");
+  k_mi_partial<<<kMiBlocks, kMiThreads, 0, s>>>(llr, bits, count, part);
+  k_mi_final<<<1, kMiThreads, 0, s>>>(part, kMiBlocks, count, out);
+  e = cudaGetLastError();
+  cudaFreeAsync(part, s);
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "exit_mutual_information");
 }
 
 int ls_count_errors(const uint8_t *b, const uint8_t *b_hat, int64_t batch, int64_t len,

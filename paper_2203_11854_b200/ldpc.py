@@ -6,10 +6,15 @@
 * `bp_decode` runs the EXACT-mode GPU decoder on any ParityCheckMatrix:
   bit-identical to the reference for min-sum / scaled-min-sum, and the
   reference's precision pattern for sum-product (LLRs within tolerance).
-* `ldpc5g_decode(..., mode="exact")` (default) is derate_match + exact BP;
-  `mode="fast"` is the on-chip QC decoder fused with rate matching, hard
-  decision and error counting (fp32, statistically equivalent; hard
-  decisions identical on every block that converges).
+  On a lifted 5G code's pcm the min-sum variants take the on-chip QC exact
+  decoder (bp_qc_exact.cuh), anything else the HBM-streaming CSR engine.
+* `ldpc5g_decode(..., mode="exact")` (default) is derate_match + exact BP
+  (fused into the on-chip decoder for min-sum on f32 LLRs); `mode="fast"`
+  is the on-chip QC decoder fused with rate matching, hard decision and
+  error counting: fp16x2 by default ("auto"; two codewords per 32-bit lane,
+  dead extension rows pruned), or precision "fp32-full" (f32 messages, all
+  rows) / "fp32" (legacy f32 kernel) -- statistically equivalent, hard
+  decisions identical on every block that converges.
 """
 from __future__ import annotations
 
@@ -21,7 +26,6 @@ import numpy as np
 from . import _lib as L
 from .alist import ParityCheckMatrix
 from .basegraph import base_graph
-from .core import LLR_MAX
 
 BP_VARIANTS = ("sum-product", "min-sum", "scaled-min-sum")
 _VARIANT_ID = {v: i for i, v in enumerate(BP_VARIANTS)}
@@ -364,14 +368,14 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
 
 
 def exit_mutual_information(llr, bits) -> float:
-    """I = 1 - E[log2(1 + exp(-(2b-1) L))] clipped to [0, 1] (ldpc.py:175-188)."""
-    torch = L.torch()
-    tl = L.to_device(llr, "float64")
-    tb = L.to_device(bits, "float64")
+    """I = 1 - E[log2(1 + exp(-(2b-1) L))] clipped to [0, 1] (ldpc.py:175-188),
+    f64 on the GPU (k_mi_partial / k_mi_final)."""
+    tl = L.to_device(llr, "float64").contiguous()
+    tb = L.to_device(bits, "float64").contiguous()
     if tl.numel() == 0:
         raise ValueError("exit_mutual_information: empty input")
     if tuple(tl.shape) != tuple(tb.shape):
         raise ValueError("exit_mutual_information: shape mismatch")
-    x = torch.clamp(-(2.0 * tb - 1.0) * tl, -LLR_MAX, LLR_MAX)
-    info = 1.0 - torch.mean(torch.log2(1.0 + torch.exp(x)))
-    return float(torch.clamp(info, 0.0, 1.0))
+    out = L.empty((1,), "float64")
+    L.call("ls_exit_mutual_information", L.ptr(tl), L.ptr(tb), tl.numel(), L.ptr(out), L.stream_ptr())
+    return float(out.cpu()[0])

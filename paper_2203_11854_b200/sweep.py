@@ -174,11 +174,23 @@ class Pipeline:
                 raise ConfigError("code.decoder.variant", f"unknown variant {variant!r}")
             self.bp_variant = variant
             self.bp_iter = dec.get("num_iter", 20)
-            self.bp_scale = dec.get("scale", 0.75)
-            self.bp_early_stop = dec.get("early_stop", True)
             self.decoder_mode = dec.get("mode", "exact")
             if self.decoder_mode not in ("exact", "fast"):
                 raise ConfigError("code.decoder.mode", f"unknown mode {self.decoder_mode!r}")
+            # The reference's Pipeline decodes with ldpc5g_decode's defaults
+            # (scale 0.75, early stop on) whatever the config says
+            # (sweep.py:335-336).  Exact mode keeps that drop-in behaviour;
+            # decoder.scale / decoder.early_stop are B200 fast-mode options.
+            self.bp_scale, self.bp_early_stop = 0.75, True
+            if self.decoder_mode == "fast":
+                self.bp_scale = dec.get("scale", 0.75)
+                self.bp_early_stop = dec.get("early_stop", True)
+            elif dec.get("scale", 0.75) != 0.75 or dec.get("early_stop", True) is not True:
+                import warnings
+
+                warnings.warn("code.decoder.scale / early_stop are ignored in exact mode, as by the "
+                              "reference's Pipeline (sweep.py:335-336); set decoder.mode 'fast' to use them",
+                              stacklevel=2)
             self.decoder_precision = dec.get("precision", "auto")
             if self.decoder_precision not in ("auto", "fp32", "fp16x2", "fp32-full"):
                 raise ConfigError("code.decoder.precision",

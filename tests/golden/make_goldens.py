@@ -181,6 +181,24 @@ def sweep_fixture():
                 csv_header=csv_text.splitlines()[0])
 
 
+def misc_fixture(core, ldpc):
+    """hard_decide (core.py:102-104) on signed zeros / denormals / ties, and
+    exit_mutual_information (ldpc.py:175-188) on seeded LLRs."""
+    g = np.random.default_rng(17)
+    edge = np.array([0.0, -0.0, 1e-45, -1e-45, 1.0, -1.0, 40.0, -40.0, 1e30, -1e30], np.float32)
+    bits = g.integers(0, 2, size=(6, 1000)).astype(np.uint8)
+    # consistent Gaussian LLRs L = (2b-1) mu + N(0, 2 mu), mu = 4
+    llr = (2.0 * bits - 1.0) * 4.0 + g.normal(size=bits.shape) * np.sqrt(8.0)
+    llr_sat = np.concatenate([llr, (2.0 * bits[:1] - 1.0) * 80.0])  # |x| clipped at 40
+    llr_sat[-1, :50] *= -1.0
+    bits_sat = np.concatenate([bits, bits[:1]])
+    return dict(edge=edge, edge_hard=core.hard_decide(edge), edge64_hard=core.hard_decide(edge.astype(np.float64)),
+                mi_llr=llr, mi_bits=bits, mi=np.float64(ldpc.exit_mutual_information(llr, bits)),
+                mi_llr_sat=llr_sat, mi_bits_sat=bits_sat,
+                mi_sat=np.float64(ldpc.exit_mutual_information(llr_sat, bits_sat)),
+                mi_perfect=np.float64(ldpc.exit_mutual_information(np.where(bits == 1, 30.0, -30.0), bits)))
+
+
 def encoder_fixture(core, ldpc):
     out = {}
     for i, (k, n) in enumerate([(256, 512), (8448, 16896), (4096, 8192), (4096, 12288),
@@ -255,6 +273,7 @@ def main():
                         **chain_double_fixture(core, ldpc, mapping, channel, 256, 512, 2, 2.0, 48, 42,
                                                (1 << 32) | 1, ("min-sum", "scaled-min-sum", "sum-product")))
     np.savez_compressed(os.path.join(OUT, "sweep_c1.npz"), meta=meta, **sweep_fixture())
+    np.savez_compressed(os.path.join(OUT, "misc.npz"), meta=meta, **misc_fixture(core, ldpc))
     if "--new-only" in sys.argv:
         return
     np.savez_compressed(os.path.join(OUT, "base_graphs.npz"), meta=meta, **base_graphs(ldpc))

@@ -778,3 +778,66 @@ def test_pipeline_double_precision_chain(golden, variant):
             "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"mode": "fast"}},
             "modulation": {"kind": "qam", "bits_per_symbol": m}, "precision": "double",
             "sweep": {"ebno_db": [2.0], "batch_size": B}}))
+
+
+def test_hard_decide_kernel(golden):
+    """core.py:102-104 on the GPU: ties and -0.0 decide 0, f32 and f64."""
+    d = golden("misc")
+    assert np.array_equal(lb.hard_decide(d["edge"]), d["edge_hard"])
+    assert np.array_equal(lb.hard_decide(d["edge"].astype(np.float64)), d["edge64_hard"])
+    x = np.random.default_rng(4).normal(size=(37, 1001)).astype(np.float32)
+    x[0, :5] = [0.0, -0.0, np.nan, np.inf, -np.inf]
+    assert np.array_equal(lb.hard_decide(x), O.hard_decide(x))
+    t = torch.from_numpy(x).cuda()
+    assert torch.equal(lb.hard_decide(t).cpu(), torch.from_numpy(O.hard_decide(x)))
+
+
+def test_exit_mutual_information_kernel(golden):
+    """ldpc.py:175-188 on the GPU (deterministic f64 reduction): within 1e-12
+    of the reference's value, saturation and the clip to [0, 1] included."""
+    d = golden("misc")
+    assert abs(lb.exit_mutual_information(d["mi_llr"], d["mi_bits"]) - float(d["mi"])) < 1e-12
+    assert abs(lb.exit_mutual_information(d["mi_llr_sat"], d["mi_bits_sat"]) - float(d["mi_sat"])) < 1e-12
+    bits = d["mi_bits"]
+    assert abs(lb.exit_mutual_information(np.where(bits == 1, 30.0, -30.0), bits) - float(d["mi_perfect"])) < 1e-12
+    assert lb.exit_mutual_information(-d["mi_llr"], bits) == 0.0  # clipped at 0
+    big = np.random.default_rng(2).normal(size=(300, 4096)) * 3.0
+    bb = (np.random.default_rng(3).random((300, 4096)) < 0.5).astype(np.uint8)
+    assert abs(lb.exit_mutual_information(big, bb) - O.exit_mutual_information(big, bb)) < 1e-12
+    with pytest.raises(ValueError):
+        lb.exit_mutual_information(np.zeros((0,)), np.zeros((0,)))
+    with pytest.raises(ValueError):
+        lb.exit_mutual_information(np.zeros((2, 3)), np.zeros((3, 2)))
+
+
+def _high_degree_pcm(seed=5):
+    """A generic graph with a 150-edge check, a 90-edge variable and a
+    200-edge check (beyond the 128-term block of numpy's pairwise sum)."""
+    g = np.random.default_rng(seed)
+    n, m = 700, 220
+    h = np.zeros((m, n), np.uint8)
+    for c in range(m):
+        h[c, g.choice(n, 6, replace=False)] = 1
+    h[0, g.choice(n, 150, replace=False)] = 1
+    h[1, g.choice(n, 200, replace=False)] = 1
+    h[g.choice(m, 90, replace=False), 3] = 1
+    return lb.ParityCheckMatrix.from_dense(h), h
+
+
+@pytest.mark.parametrize("variant", ["min-sum", "scaled-min-sum", "sum-product"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_bp_exact_high_degree_nodes(variant, dt):
+    """No degree cap: nodes above 64 edges stream over their edges (two passes
+    per check, streaming pairwise sums incl. numpy's >128-term split)."""
+    pcm, h = _high_degree_pcm()
+    assert h.sum(axis=1).max() == 200 or h.sum(axis=1).max() > 128
+    g = np.random.default_rng(8)
+    llr = (g.normal(size=(64, pcm.n)) * 2.0 + 1.5).astype(dt)
+    ptr, var = pcm.csr()
+    lo, hard, it = lb.bp_decode(llr, pcm, 12, variant, 0.75, True, return_iters=True)
+    lo_o, hard_o, it_o = O.bp_decode_csr(llr, ptr, var, pcm.n, 12, variant, 0.75, True)
+    assert np.array_equal(hard, hard_o) and np.array_equal(it, it_o)
+    if variant == "sum-product":
+        assert np.allclose(lo, lo_o, rtol=1e-4, atol=1e-4)
+    else:
+        assert np.array_equal(lo, lo_o)

@@ -148,3 +148,11 @@ def test_run_batch_chain_c1(golden):
     payload, dec = O.run_batch(k, n, m, 2.0, B, 42, (1 << 32) | 1, "sum-product")
     assert np.array_equal(np.packbits(payload, axis=-1), d["payload"])
     assert np.array_equal(np.packbits(dec, axis=-1), d["sum_product_decoded"])
+
+
+def test_oracle_hard_decide_and_exit_mi(golden):
+    d = golden("misc")
+    assert np.array_equal(O.hard_decide(d["edge"]), d["edge_hard"])
+    assert np.array_equal(O.hard_decide(d["edge"].astype(np.float64)), d["edge64_hard"])
+    assert O.exit_mutual_information(d["mi_llr"], d["mi_bits"]) == float(d["mi"])
+    assert O.exit_mutual_information(d["mi_llr_sat"], d["mi_bits_sat"]) == float(d["mi_sat"])
