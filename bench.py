@@ -299,6 +299,10 @@ def run_b200(a, rank, world, local_rank):
         line["fast_fp16x2_min_sum"] = fast_rate(a, rank, world, dist, "fp16x2", prune=True)
         line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32-full", prune=False)
         line["sum_product_fast"] = sum_product_rate(a, rank, world, dist)
+        line["config3_sweep"] = config3_sweep(a, rank, world, dist)
+        line["config4_demappers"] = config4_demappers(a, rank, world, dist)
+        if rank == 0:
+            line["config5_decoder_only"] = config5_decoder_only(a)
     if rank == 0 and world == 1 and not a.no_cpu:
         v, cw, el = cpu_chain_rate(a, a.cpu_seconds, os.cpu_count() or 1)
         line["cpu_baseline"] = dict({"value": v, "unit": "Gbit/s", "cores": os.cpu_count() or 1, "kind": "port",
@@ -342,11 +346,13 @@ def host_info():
     return info
 
 
-def _timed_steps(fn, steps, dist):
+def _timed_steps(fn, steps, dist, reset=None):
     import torch
 
     fn(-1)
     torch.cuda.synchronize()
+    if reset:
+        reset()
     if dist:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -380,7 +386,7 @@ def exact_early_stop_rate(a, pipe, rank, world, dist, steps=3):
                          want_hard=False, want_iters=True, counts=counts, precision="exact")
         iters.append(r["iters"])
 
-    ms, clk = _timed_steps(one, steps, dist)
+    ms, clk = _timed_steps(one, steps, dist, reset=counts.zero_)
     mean_it = float(torch.cat(iters[1:]).float().mean())
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s",
             "mean_iterations": mean_it, "ms_per_step": ms / steps, "clocks": clk,
@@ -420,7 +426,7 @@ def fast_rate(a, rank, world, dist, precision, prune, steps=3):
         d1.record()
         dec.append((d0, d1))
 
-    ms, clk = _timed_steps(one, steps, dist)
+    ms, clk = _timed_steps(one, steps, dist, reset=counts.zero_)
     dms = sum(d0.elapsed_time(d1) for d0, d1 in dec[1:]) / steps
     c = counts.cpu().tolist()
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
@@ -456,13 +462,114 @@ def sum_product_rate(a, rank, world, dist, steps=2):
         d1.record()
         dec.append((d0, d1))
 
-    ms, clk = _timed_steps(one, steps, dist)
+    ms, clk = _timed_steps(one, steps, dist, reset=counts.zero_)
     dms = sum(d0.elapsed_time(d1) for d0, d1 in dec[1:]) / steps
     c = counts.cpu().tolist()
     return {"value": world * B * K_INFO * steps / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / steps,
             "decoder_ms_per_launch": dms, "bit_errors": c[0], "block_errors": c[1], "clocks": clk,
             "note": "sum-product, fixed iterations, k_qc_sp (fp16 messages in shared memory, fp32 base-2 phi, "
                     "product-domain check update); fast mode, statistically equivalent"}
+
+
+def config3_sweep(a, rank, world, dist):
+    """BASELINE config 3: error-count-stopped Eb/N0 sweep, BG1 k=4096 r=1/2
+    QPSK, exact decoder (the reference's arithmetic), waves of batches sharded
+    over the ranks (sweep.py:411-476).  Bounded: 4 batches of 8,192 per point."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    cfg = lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": 4096, "n": 8192, "decoder": {"variant": "min-sum", "num_iter": 20}},
+        "modulation": {"kind": "qam", "bits_per_symbol": 2},
+        "sweep": {"ebno_db": [0.0, 1.0, 2.0, 3.0, 4.0, 5.0, 6.0], "batch_size": 8192,
+                  "target_block_errors": 100, "max_batches_per_point": 4}, "seed": 2024})
+    lb.run_sweep(lb.SimConfig.from_dict({  # warm-up (handles, workspaces)
+        "code": cfg.code, "modulation": cfg.modulation,
+        "sweep": {"ebno_db": [3.0], "batch_size": 8192, "max_batches_per_point": 1}}), num_workers=4)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t = time.perf_counter()
+    res = lb.run_sweep(cfg, num_workers=4 * world)
+    torch.cuda.synchronize()
+    el = _wall_max(dist, time.perf_counter() - t)
+    bits = sum(p.bits for p in res.points)
+    return {"value": bits / el / 1e9, "unit": "Gbit/s", "decoded_bits": bits, "elapsed_s": el,
+            "points": [[p.ebno_db, p.blocks, p.block_errors, p.bit_errors, p.stop_reason] for p in res.points],
+            "note": "run_sweep, exact mode (numpy-exact noise, on-chip exact decoder, Z=192: two CTAs per SM); "
+                    "statistics identical for any rank count; wall clock incl. host orchestration"}
+
+
+def config4_demappers(a, rank, world, dist, B=131072):
+    """BASELINE config 4: 64-QAM APP vs max-log, BG1 k=4096 n=12288 (r=1/3,
+    fillers, puncturing), batch 131,072, exact chain."""
+    import paper_2203_11854_b200 as lb
+    from paper_2203_11854_b200 import _lib as L
+
+    out = {}
+    for demapper in ("app", "maxlog"):
+        pipe = lb.Pipeline(lb.SimConfig.from_dict({
+            "code": {"family": "ldpc5g", "k": 4096, "n": 12288, "decoder": {"variant": "min-sum", "num_iter": 20}},
+            "modulation": {"kind": "qam", "bits_per_symbol": 6, "demapper": demapper},
+            "sweep": {"ebno_db": [7.5], "batch_size": B}, "seed": 7}))
+        counts = L.zeros((2,), "int64")
+
+        def one(i):
+            pipe.run_batch_counts(7.5, B, lb.RngStream(7, ((rank + 1) << 40) | (20 + i)), counts)
+
+        ms, clk = _timed_steps(one, 2, dist, reset=counts.zero_)
+        c = counts.cpu().tolist()
+        out[demapper] = {"value": world * B * 4096 * 2 / (ms / 1e3) / 1e9, "unit": "Gbit/s", "ms_per_step": ms / 2,
+                         "bit_errors": c[0], "block_errors": c[1], "blocks": 2 * B, "clocks": clk}
+    out["note"] = "exact chain at 7.5 dB (numpy-exact noise, f64 demapper, on-chip exact decoder, early stop on)"
+    return out
+
+
+def config5_decoder_only(a):
+    """BASELINE config 5 (subset): decoder-only throughput, min-sum vs
+    sum-product (boxplus), 5/20/50 iterations, BG1 and BG2 at Z = 64..384."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    rows = []
+    for bg, z in ((1, 64), (1, 192), (1, 384), (2, 64), (2, 384)):
+        kb = 22 if bg == 1 else 10
+        k = kb * z
+        n = 2 * k if bg == 1 else 3 * k
+        code = lb.LdpcCode5G(k, n, base_graph=bg, z=z)
+        B = max(1024, (1 << 27) // k)
+        cfgd = {"code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"mode": "fast"}},
+                "modulation": {"kind": "qam", "bits_per_symbol": 2}, "sweep": {"ebno_db": [4.0], "batch_size": B}}
+        pipe = lb.Pipeline(lb.SimConfig.from_dict(cfgd))
+        pipe.ldpc = code
+        payload, llr = pipe._llr(4.0 if bg == 1 else 5.0, B, lb.RngStream(5, z))
+        kinds = [("min-sum", "fp16x2"), ("sum-product", "fp32")]
+        if lb.ldpc.qc_has_kernel(code, precision="exact"):
+            kinds += [("min-sum", "exact"), ("min-sum", "fp32-full")]
+        for variant, prec in kinds:
+            for it in (5, 20, 50):
+                def run():
+                    return lb.qc_decode(llr, code, it, variant, 0.75, early_stop=False, want_hard=False,
+                                        ref_bits=payload, precision=prec)
+                try:
+                    run()
+                except ValueError as e:  # no instance for this geometry
+                    rows.append({"bg": bg, "z": z, "variant": variant, "precision": prec, "iters": it,
+                                 "skipped": str(e)})
+                    continue
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                rows.append({"bg": bg, "z": z, "k": k, "n": n, "variant": variant, "precision": prec, "iters": it,
+                             "batch": B, "ms": ms, "gbit_s": B * k / (ms / 1e3) / 1e9})
+    return {"rows": rows, "note": "decoder only on device-resident LLRs (fast modem), fixed iterations; BG2 at "
+                                  "Z >= 32 is the harness-lifted graph (LdpcCode5G(k, n, base_graph=2, z=Z))"}
 
 
 def _wall_max(dist, secs):
