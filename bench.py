@@ -29,13 +29,14 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 K_INFO, N_TX, M_BITS = 8448, 16896, 4
-# kernels of one headline step (ncu launch list, profiles/r02/launches_bench.csv):
-# binary_source, encoder, mapper, 5 numpy-ziggurat kernels, demapper, exact decoder
-GPU_LAUNCHES_PER_STEP = 10
+# kernels of one headline step (ncu launch list, profiles/r02/launches_bench_r2.csv):
+# binary_source, encoder, mapper, 5 numpy-ziggurat kernels, noise apply, demapper, exact decoder
+GPU_LAUNCHES_PER_STEP = 11
 # DRAM bytes (read + write) per codeword of k_qc_exact<BG1,384,2>, from the
-# ncu --set full capture of the bench's own decoder launch (profiles/r02/);
+# ncu --set full capture of the bench's own 65,536-codeword decoder launch
+# (profiles/r02/ncu_k_qc_exact_bench_*: 5.103 GB read + 0.125 GB written);
 # the messages never leave the SM, DRAM sees the LLR input and the counts
-EXACT_TRAFFIC_PER_CW = 94_468_608 / 1184
+EXACT_TRAFFIC_PER_CW = (5_103_239_000 + 125_331_712) / 65536
 METRIC = "decoded info Gbit/s (LDPC BG1, 20 iters) at 1/2/4/8 B200 vs CPU ref; %roofline"
 
 
