@@ -281,7 +281,14 @@ class Pipeline:
         torch = L.torch()
         if batch_size <= chunk or self.noise == "numpy":  # the numpy stream is drawn per batch
             p, d = self.run_batch_device(ebno_db, batch_size, rng)
-            return L.to_host(p), L.to_host(d)
+            # pinned outputs from torch's caching host allocator: one fast D2H
+            # each, and the numpy arrays keep their buffers alive
+            ph = torch.empty(tuple(p.shape), dtype=p.dtype, pin_memory=True)
+            dh = torch.empty(tuple(d.shape), dtype=d.dtype, pin_memory=True)
+            ph.copy_(p, non_blocking=True)
+            dh.copy_(d, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return ph.numpy(), dh.numpy()
         chunk = max(32, (chunk // 32) * 32)
         k = self.payload_bits
         ph = torch.empty((batch_size, k), dtype=torch.uint8, pin_memory=True)
