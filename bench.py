@@ -289,6 +289,11 @@ def run_b200(a, rank, world, local_rank):
                                   note="messages stay on chip (f64 min1 + argmin/sign words in shared memory, "
                                        "min2 and channel in an L2 slice per SM); the kernel is bound by the "
                                        "ALU issue pipe, not HBM (ncu in profiles/r02)"),
+            "issue_roofline": {"note": "from the ncu --set full capture of this decoder launch at B=65,536 "
+                                       "(profiles/r02/ncu_k_qc_exact_bench_summary.txt)",
+                               "warp_instructions_per_launch": 185_036_924_212, "ipc": 2.69, "ipc_peak": 4.0,
+                               "issue_frac": 2.69 / 4.0, "alu_pipe_frac": 0.711,
+                               "dram_bytes_per_launch": 5_228_570_712},
             "clocks": clk.summary(),
             "errors_in_timed_region": {"bit_errors": errs[0], "block_errors": errs[1],
                                        "blocks": world * B * a.steps}}
