@@ -313,6 +313,38 @@ struct QamAxes {
   int lab[16];      // axis label of each level, MSB first
 };
 
+// e^x for x <= 0 (the demapper's exp(logit - max)): x = k ln2 + r, |r| <=
+// ln2/2, degree-13 Taylor for e^r (truncation < 2e-16 relative), times 2^k.
+// Below -708 the reference's value is subnormal or zero, far under the f64
+// resolution of the LLR it enters (log1p(t) ~ t added to a max term), so 0.
+// coefficients in the constant bank: DFMA reads them as operands (as
+// constexpr locals every use costs two UMOVs)
+__constant__ double dm_exp_c[14] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333, 0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10};
+__constant__ double dm_atanh_c[16] = {1.0, 0.3333333333333333, 0.2, 0.14285714285714285, 0.1111111111111111, 0.09090909090909091, 0.07692307692307693, 0.06666666666666667, 0.058823529411764705, 0.05263157894736842, 0.047619047619047616, 0.043478260869565216, 0.04, 0.037037037037037035, 0.034482758620689655, 0.03225806451612903};
+
+__device__ __forceinline__ double dm_exp_neg(double x) {
+  if (x < -708.0) return 0.0;
+  const double kd = rint(x * 1.4426950408889634);
+  const double r = fma(kd, -1.9082149292705877e-10, fma(kd, -6.93147180369123816490e-01, x));
+  double p = dm_exp_c[13];
+#pragma unroll
+  for (int n = 12; n >= 0; --n) p = fma(p, r, dm_exp_c[n]);
+  return p * __hiloint2double(((int)kd + 1023) << 20, 0);
+}
+
+// log1p(t) for 0 <= t <= 1 (the log-sum-exp tail of a 2-level set):
+// 2 atanh(z), z = t / (2 + t) <= 1/3, atanh(z)/z as its Taylor series in
+// w = z^2 <= 1/9 to degree 15 (truncation < 5e-17); larger t (64/256-QAM sets
+// of 4 or more levels) take the library log1p.
+__device__ __forceinline__ double dm_log1p(double t) {
+  if (t > 1.0) return log1p(t);
+  const double z = t / (2.0 + t), w = z * z;
+  double p = dm_atanh_c[15];
+#pragma unroll
+  for (int k = 14; k >= 0; --k) p = fma(p, w, dm_atanh_c[k]);
+  return 2.0 * z * p;
+}
+
 template <int HALF, class YT>
 __global__ void k_demap_qam(const YT *__restrict__ y, int64_t nsym, double no,
                             const double *__restrict__ no_vec, const double *__restrict__ prior,
@@ -361,14 +393,75 @@ __global__ void k_demap_qam(const YT *__restrict__ y, int64_t nsym, double no,
 #pragma unroll
           for (int l = 0; l < L; ++l) {
             if ((A.lab[l] >> sh) & 1) {
-              if (l != a1) s1 += exp(lg[l] - mx1);
+              if (l != a1) s1 += dm_exp_neg(lg[l] - mx1);
             } else {
-              if (l != a0) s0 += exp(lg[l] - mx0);
+              if (l != a0) s0 += dm_exp_neg(lg[l] - mx0);
             }
           }
-          v = (mx1 + log1p(s1)) - (mx0 + log1p(s0));
+          v = (mx1 + dm_log1p(s1)) - (mx0 + dm_log1p(s0));
         }
         out[2 * t + ax] = v;  // stream bit 2t is the t-th I bit, 2t+1 the t-th Q bit
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      if (llr32) llr32[s * M + j] = (float)out[j];
+      if (llr64) llr64[s * M + j] = out[j];
+    }
+  }
+}
+
+// Gray QAM without priors (the sweep engine's case): the same arithmetic with
+// the Gray labels l ^ (l >> 1) compile-time, so every bit's two level sets,
+// their maxima and the log-sum-exp tails are straight-line code
+template <int HALF, int MODE, class YT>
+__global__ void __launch_bounds__(256) k_demap_qam_gray(const YT *__restrict__ y, int64_t nsym, double no,
+                                                        const double *__restrict__ no_vec, const QamAxes A,
+                                                        float *__restrict__ llr32, double *__restrict__ llr64) {
+  constexpr int L = 1 << HALF, M = 2 * HALF;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsym;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const double2 ys = ld_sym(y, s);
+    const double inv = 1.0 / (no_vec ? no_vec[s] : no);
+    double out[M];
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      const double yv = ax == 0 ? (double)ys.x : (double)ys.y;
+      double lg[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const double d = yv - A.amp[l];
+        lg[l] = -(d * d) * inv;
+      }
+#pragma unroll
+      for (int t = 0; t < HALF; ++t) {
+        double lse[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          // levels whose Gray label has bit t (MSB first) equal to b
+          double mx = -INFINITY;
+          int arg = 0;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            if ((((l ^ (l >> 1)) >> (HALF - 1 - t)) & 1) != b) continue;
+            if (lg[l] > mx) {
+              mx = lg[l];
+              arg = l;
+            }
+          }
+          if (MODE == LS_DEMAP_MAXLOG) {
+            lse[b] = mx;
+          } else {
+            double sum = 0.0;
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+              if ((((l ^ (l >> 1)) >> (HALF - 1 - t)) & 1) != b) continue;
+              sum += l == arg ? 0.0 : dm_exp_neg(lg[l] - mx);
+            }
+            lse[b] = mx + dm_log1p(sum);
+          }
+        }
+        out[2 * t + ax] = lse[1] - lse[0];
       }
     }
 #pragma unroll
@@ -807,6 +900,23 @@ static int demap_qam_any(const YT *yy, int64_t nsym, double no, const double *no
   }
   cudaStream_t s = as_stream(stream);
   const unsigned g = grid_for(nsym, 256);
+  bool gray = !prior && (m == 4 || m == 6);
+  for (int l = 0; l < L; ++l) gray = gray && lab[l] == (l ^ (l >> 1));
+  if (gray) {
+    if (m == 4) {
+      if (mode == LS_DEMAP_APP)
+        k_demap_qam_gray<2, LS_DEMAP_APP><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, llr32, llr64);
+      else
+        k_demap_qam_gray<2, LS_DEMAP_MAXLOG><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, llr32, llr64);
+    } else {
+      if (mode == LS_DEMAP_APP)
+        k_demap_qam_gray<3, LS_DEMAP_APP><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, llr32, llr64);
+      else
+        k_demap_qam_gray<3, LS_DEMAP_MAXLOG><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, A, llr32, llr64);
+    }
+    LS_CHECK_LAUNCH("ls_demap_qam");
+    return LS_OK;
+  }
   switch (m) {
     case 2: k_demap_qam<1><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
     case 4: k_demap_qam<2><<<g, 256, 0, s>>>(yy, nsym, no, no_vec, prior, A, mode, llr32, llr64); break;
