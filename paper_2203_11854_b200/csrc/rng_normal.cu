@@ -143,41 +143,29 @@ __device__ double zig_draw(uint64_t seed, uint64_t sid, int64_t p, int *len) {
   }
 }
 
-// sort the specials of a segment by position (thread 0; ~8 entries)
-__device__ __forceinline__ void zig_sort(uint16_t *spos, uint16_t *slen, double *sval, int n) {
-  for (int i = 1; i < n; ++i) {
-    const uint16_t p = spos[i], l = slen[i];
-    const double v = sval ? sval[i] : 0.0;
-    int j = i - 1;
-    while (j >= 0 && spos[j] > p) {
-      spos[j + 1] = spos[j];
-      slen[j + 1] = slen[j];
-      if (sval) sval[j + 1] = sval[j];
-      --j;
-    }
-    spos[j + 1] = p;
-    slen[j + 1] = l;
-    if (sval) sval[j + 1] = v;
-  }
-}
-
 // Multi-word ("special") draws of a segment, evaluated CONVERGED: the
-// positions are collected first, then one lane per special walks the slow
-// path, so a warp runs the wedge / tail code once instead of once per lane
-// that happens to hold a special word.
-__device__ __forceinline__ void zig_eval_specials(uint64_t seed, uint64_t sid, int64_t base, uint16_t *spos,
-                                                  uint16_t *slen, double *sval, int n) {
+// positions are collected first (unsorted, spos_u), then one lane per special
+// walks the slow path, so a warp runs the wedge / tail code once instead of
+// once per lane that happens to hold a special word.  The same lane writes its
+// special at its rank (number of specials at smaller positions) into the
+// position-sorted arrays: no serial sort.
+__device__ __forceinline__ void zig_eval_specials(uint64_t seed, uint64_t sid, int64_t base, const uint16_t *spos_u,
+                                                  uint16_t *spos, uint16_t *slen, double *sval, int n) {
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int pk = spos_u[k];
     int len;
-    const double v = zig_draw(seed, sid, base + spos[k], &len);
-    slen[k] = (uint16_t)min(len, 65535);
-    if (sval) sval[k] = v;
+    const double v = zig_draw(seed, sid, base + pk, &len);
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += spos_u[j] < pk;
+    spos[rank] = (uint16_t)pk;
+    slen[rank] = (uint16_t)min(len, 65535);
+    if (sval) sval[rank] = v;
   }
 }
 
 // specials of segment s (sorted by position), shared by the segment kernels
-__device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *spos, uint16_t *slen,
-                            int *count, int *overflow) {
+__device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *spos_u, uint16_t *spos,
+                            uint16_t *slen, int *count, int *overflow) {
   const int t = threadIdx.x;
   if (t == 0) *count = 0;
   __syncthreads();
@@ -192,7 +180,7 @@ __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *sp
       if (!(rabs < ls_zig_ki[w[u] & 0xff])) {
         const int k = atomicAdd(count, 1);
         if (k < kZSpec)
-          spos[k] = (uint16_t)(4 * b + u);
+          spos_u[k] = (uint16_t)(4 * b + u);
         else
           *overflow = 1;
       }
@@ -200,9 +188,7 @@ __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *sp
   }
   __syncthreads();
   const int n = min(*count, kZSpec);
-  zig_eval_specials(seed, sid, base, spos, slen, nullptr, n);
-  __syncthreads();
-  if (t == 0) zig_sort(spos, slen, nullptr, n);
+  zig_eval_specials(seed, sid, base, spos_u, spos, slen, nullptr, n);
   __syncthreads();
   return n;
 }
@@ -226,10 +212,10 @@ __device__ __forceinline__ void zig_walk(const uint16_t *spos, const uint16_t *s
 
 __global__ void k_zig_segments(uint64_t seed, uint64_t sid, int64_t nseg, uint32_t *__restrict__ trans,
                                int *__restrict__ overflow) {
-  __shared__ uint16_t spos[kZSpec], slen[kZSpec];
+  __shared__ uint16_t spos_u[kZSpec], spos[kZSpec], slen[kZSpec];
   __shared__ int count;
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
-    const int n = zig_specials(seed, sid, s, spos, slen, &count, overflow);
+    const int n = zig_specials(seed, sid, s, spos_u, spos, slen, &count, overflow);
     const int e = threadIdx.x;
     if (e < kZK) {
       int cnt, cur;
@@ -301,7 +287,7 @@ __global__ void k_zig_assign(const uint32_t *__restrict__ trans, int64_t nseg, i
 __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, int64_t nseg,
                                                   const int *__restrict__ sentry, const int64_t *__restrict__ sbase,
                                                   int64_t count, double *__restrict__ out, int *__restrict__ overflow) {
-  __shared__ uint16_t spos[kZSpec], slen[kZSpec];
+  __shared__ uint16_t spos_u[kZSpec], spos[kZSpec], slen[kZSpec];
   __shared__ double sval[kZSpec];
   __shared__ int cnt_s;
   const int t = threadIdx.x;
@@ -326,16 +312,14 @@ __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, i
         spec |= 1u << u;
         const int k = atomicAdd(&cnt_s, 1);
         if (k < kZSpec)
-          spos[k] = (uint16_t)(4 * t + u);
+          spos_u[k] = (uint16_t)(4 * t + u);
         else
           *overflow = 1;
       }
     }
     __syncthreads();
     const int n = min(cnt_s, kZSpec);
-    zig_eval_specials(seed, sid, s * kZG, spos, slen, sval, n);
-    __syncthreads();
-    if (t == 0) zig_sort(spos, slen, sval, n);
+    zig_eval_specials(seed, sid, s * kZG, spos_u, spos, slen, sval, n);
     __syncthreads();
     const int e = sentry[s];
     int cnt, cur;
