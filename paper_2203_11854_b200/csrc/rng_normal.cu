@@ -32,6 +32,7 @@ constexpr int kZG = 1024;     // words per segment
 constexpr int kZK = 32;       // entry offsets tracked per segment
 constexpr int kZSpec = 96;    // max multi-word starts per segment
 constexpr int kZGroup = 512;  // segments per scan group
+constexpr int kZCache = 32;   // specials per segment handed from the scan pass to the emit pass
 
 __device__ __forceinline__ uint64_t word_at(uint64_t seed, uint64_t sid, int64_t p) {
   uint64_t w[4];
@@ -165,7 +166,7 @@ __device__ __forceinline__ void zig_eval_specials(uint64_t seed, uint64_t sid, i
 
 // specials of segment s (sorted by position), shared by the segment kernels
 __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *spos_u, uint16_t *spos,
-                            uint16_t *slen, int *count, int *overflow) {
+                            uint16_t *slen, double *sval, int *count, int *overflow) {
   const int t = threadIdx.x;
   if (t == 0) *count = 0;
   __syncthreads();
@@ -188,7 +189,7 @@ __device__ int zig_specials(uint64_t seed, uint64_t sid, int64_t s, uint16_t *sp
   }
   __syncthreads();
   const int n = min(*count, kZSpec);
-  zig_eval_specials(seed, sid, base, spos_u, spos, slen, nullptr, n);
+  zig_eval_specials(seed, sid, base, spos_u, spos, slen, sval, n);
   __syncthreads();
   return n;
 }
@@ -210,12 +211,22 @@ __device__ __forceinline__ void zig_walk(const uint16_t *spos, const uint16_t *s
   *cur_out = cur;
 }
 
+// scan pass: per segment the transfer function, and the sorted specials
+// (position | length << 16, value) for the emit pass, which then needs no
+// slow-path draw of its own when the segment has at most kZCache of them
 __global__ void k_zig_segments(uint64_t seed, uint64_t sid, int64_t nseg, uint32_t *__restrict__ trans,
-                               int *__restrict__ overflow) {
+                               int *__restrict__ overflow, uint32_t *__restrict__ ccnt,
+                               uint32_t *__restrict__ cpl, double *__restrict__ cval) {
   __shared__ uint16_t spos_u[kZSpec], spos[kZSpec], slen[kZSpec];
+  __shared__ double sval[kZSpec];
   __shared__ int count;
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
-    const int n = zig_specials(seed, sid, s, spos_u, spos, slen, &count, overflow);
+    const int n = zig_specials(seed, sid, s, spos_u, spos, slen, sval, &count, overflow);
+    if (threadIdx.x == 0) ccnt[s] = (uint32_t)n;
+    if ((int)threadIdx.x < n && n <= kZCache) {
+      cpl[s * kZCache + threadIdx.x] = (uint32_t)spos[threadIdx.x] | ((uint32_t)slen[threadIdx.x] << 16);
+      cval[s * kZCache + threadIdx.x] = sval[threadIdx.x];
+    }
     const int e = threadIdx.x;
     if (e < kZK) {
       int cnt, cur;
@@ -286,7 +297,9 @@ __global__ void k_zig_assign(const uint32_t *__restrict__ trans, int64_t nseg, i
 // re-read the stream.
 __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, int64_t nseg,
                                                   const int *__restrict__ sentry, const int64_t *__restrict__ sbase,
-                                                  int64_t count, double *__restrict__ out, int *__restrict__ overflow) {
+                                                  int64_t count, double *__restrict__ out, int *__restrict__ overflow,
+                                                  const uint32_t *__restrict__ ccnt, const uint32_t *__restrict__ cpl,
+                                                  const double *__restrict__ cval) {
   __shared__ uint16_t spos_u[kZSpec], spos[kZSpec], slen[kZSpec];
   __shared__ double sval[kZSpec];
   __shared__ int cnt_s;
@@ -319,7 +332,16 @@ __global__ void __launch_bounds__(256) k_zig_emit(uint64_t seed, uint64_t sid, i
     }
     __syncthreads();
     const int n = min(cnt_s, kZSpec);
-    zig_eval_specials(seed, sid, s * kZG, spos_u, spos, slen, sval, n);
+    if (ccnt[s] == (uint32_t)n && n <= kZCache) {  // handed over by the scan pass
+      if (t < n) {
+        const uint32_t pl = cpl[s * kZCache + t];
+        spos[t] = (uint16_t)(pl & 0xFFFFu);
+        slen[t] = (uint16_t)(pl >> 16);
+        sval[t] = cval[s * kZCache + t];
+      }
+    } else {
+      zig_eval_specials(seed, sid, s * kZG, spos_u, spos, slen, sval, n);
+    }
     __syncthreads();
     const int e = sentry[s];
     int cnt, cur;
@@ -382,7 +404,9 @@ static int normals(uint64_t seed, uint64_t sid, int64_t count, double *out, cuda
   const size_t sz_trans = sizeof(uint32_t) * nseg * kZK, sz_gx = sizeof(uint32_t) * ngroups * kZK,
                sz_gc = sizeof(int64_t) * ngroups * kZK, sz_ge = sizeof(int) * ngroups,
                sz_gb = sizeof(int64_t) * ngroups, sz_se = sizeof(int) * nseg, sz_sb = sizeof(int64_t) * nseg;
-  const size_t total = sz_trans + sz_gx + sz_gc + sz_ge + sz_gb + sz_se + sz_sb + 64;
+  const size_t sz_cc = sizeof(uint32_t) * nseg, sz_cp = sizeof(uint32_t) * nseg * kZCache,
+               sz_cv = sizeof(double) * nseg * kZCache;
+  const size_t total = sz_trans + sz_gx + sz_gc + sz_ge + sz_gb + sz_se + sz_sb + sz_cc + sz_cp + sz_cv + 160;
   cudaError_t e = cudaMallocAsync((void **)&ws, total, s);
   if (e != cudaSuccess) return cuda_status(e, "ls_standard_normal(workspace)");
   char *p = ws;
@@ -398,15 +422,18 @@ static int normals(uint64_t seed, uint64_t sid, int64_t count, double *out, cuda
   int64_t *gbase = (int64_t *)take(sz_gb);
   int *sentry = (int *)take(sz_se);
   int64_t *sbase = (int64_t *)take(sz_sb);
+  uint32_t *ccnt = (uint32_t *)take(sz_cc);
+  uint32_t *cpl = (uint32_t *)take(sz_cp);
+  double *cval = (double *)take(sz_cv);
   int *flags = (int *)take(16);
   int64_t *avail = (int64_t *)(flags + 2);
   cudaMemsetAsync(flags, 0, 16, s);
   const unsigned gs = (unsigned)std::min<int64_t>(nseg, 148 * 16);
-  k_zig_segments<<<gs, 256, 0, s>>>(seed, sid, nseg, trans, flags);
+  k_zig_segments<<<gs, 256, 0, s>>>(seed, sid, nseg, trans, flags, ccnt, cpl, cval);
   k_zig_groups<<<(unsigned)ngroups, kZK, 0, s>>>(trans, nseg, gexit, gcnt);
   k_zig_top<<<1, 1, 0, s>>>(gexit, gcnt, ngroups, gentry, gbase, avail);
   k_zig_assign<<<grid_for(ngroups, 128), 128, 0, s>>>(trans, nseg, ngroups, gentry, gbase, sentry, sbase);
-  k_zig_emit<<<gs, 256, 0, s>>>(seed, sid, nseg, sentry, sbase, count, out, flags);
+  k_zig_emit<<<gs, 256, 0, s>>>(seed, sid, nseg, sentry, sbase, count, out, flags, ccnt, cpl, cval);
   int hflags[2] = {0, 0};
   int64_t havail = 0;
   cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
