@@ -305,6 +305,8 @@ def run_b200(a, rank, world, local_rank):
         line["fast_fp16x2_min_sum"] = fast_rate(a, rank, world, dist, "fp16x2", prune=True)
         line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32-full", prune=False)
         line["sum_product_fast"] = sum_product_rate(a, rank, world, dist)
+        if rank == 0:
+            line["sum_product_f32_config3"] = sum_product_f32_rate(a)
         line["config3_sweep"] = config3_sweep(a, rank, world, dist)
         line["config4_demappers"] = config4_demappers(a, rank, world, dist)
         if rank == 0:
@@ -576,6 +578,38 @@ def config5_decoder_only(a):
                              "batch": B, "ms": ms, "gbit_s": B * k / (ms / 1e3) / 1e9})
     return {"rows": rows, "note": "decoder only on device-resident LLRs (fast modem), fixed iterations; BG2 at "
                                   "Z >= 32 is the harness-lifted graph (LdpcCode5G(k, n, base_graph=2, z=Z))"}
+
+
+def sum_product_f32_rate(a, B=32768):
+    """The f32-message sum-product option (k_qc_sp32, within 1e-4 of exact
+    sum-product on converged codewords) next to the fp16-message kernel, on
+    config 3 (BG1 k=4096 r=1/2, Z=192: where f32 messages fit on chip)."""
+    import torch
+
+    import paper_2203_11854_b200 as lb
+
+    pipe = lb.Pipeline(lb.SimConfig.from_dict({
+        "code": {"family": "ldpc5g", "k": 4096, "n": 8192, "decoder": {"mode": "fast"}},
+        "modulation": {"kind": "qam", "bits_per_symbol": 2}, "sweep": {"ebno_db": [2.0], "batch_size": B}}))
+    payload, llr = pipe._llr(2.0, B, lb.RngStream(a.seed, 31))
+    out = {}
+    for prec in ("fp32-full", "fp32"):
+        def run():
+            return lb.qc_decode(llr, pipe.ldpc, a.iters, "sum-product", early_stop=False, ref_bits=payload,
+                                want_hard=False, precision=prec)
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out["f32_messages" if prec == "fp32-full" else "fp16_messages"] = {
+            "ms": ms, "gbit_s": B * 4096 / (ms / 1e3) / 1e9}
+    out["note"] = ("decoder only, 20 fixed iterations, 2.0 dB; f32 messages: k_qc_sp32 (6 MUFU per edge, "
+                   "log domain, prefix/suffix exclusive sums); fp16 messages: k_qc_sp (4 MUFU, product domain)")
+    return out
 
 
 def _wall_max(dist, secs):

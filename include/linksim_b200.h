@@ -199,7 +199,9 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
 #define LS_QC_MOTHER 32
 /* LS_QC_FULL32: the same on-chip decoder with f32 messages (fp32 full-graph
  * fast mode: f32 v2c / min tracking / variable sums, all rows, compressed
- * state wholly in shared memory); LLRs within tolerance of exact mode. */
+ * state wholly in shared memory); LLRs within tolerance of exact mode.  With
+ * variant sum-product it selects k_qc_sp32 (f32 messages, log-domain check
+ * update, the reference's f32 first pass) where its messages fit. */
 #define LS_QC_FULL32 64
 int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch, int num_iter, int variant,
                  double scale, int early_stop, int flags, uint8_t *hard_k, float *llr_out,

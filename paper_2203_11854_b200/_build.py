@@ -41,7 +41,8 @@ def _instance_sources():
     out = []
     for bg, z, r, sp, pr in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\w+)\)", text):
         name = f"qc_{pr}_{bg}_{z}_{r}.cu"
-        launcher = {"f32": "launch_qc_fast2", "h2": "launch_qc_fast_h2", "sp": "launch_qc_sp"}[pr]
+        launcher = {"f32": "launch_qc_fast2", "h2": "launch_qc_fast_h2", "sp": "launch_qc_sp",
+                    "sp32": "launch_qc_sp32"}[pr]
         body = (f'#include "{CSRC}/bp_fast_h2.cuh"\n#include "{CSRC}/bp_fast_sp.cuh"\n'
                 "namespace lsb {\n"
                 f"int qc2_{pr}_{bg}_{z}_{r}(const QcChanParams &P, const float *l, int64_t B, int it, float a, int es,\n"

@@ -220,6 +220,7 @@ LSB_QC_INSTANCES(LSB_QC_DECL)
 #define LSB_QC_PREC_f32 0
 #define LSB_QC_PREC_h2 1
 #define LSB_QC_PREC_sp 2
+#define LSB_QC_PREC_sp32 3
 #define LSB_QC_ENTRY(bg, z, r, sp, pr) {bg, z, r, LSB_QC_PREC_##pr, &qc2_##pr##_##bg##_##z##_##r},
 static const QcKernelEntry kQcKernels[] = {LSB_QC_INSTANCES(LSB_QC_ENTRY)};
 
@@ -297,14 +298,15 @@ extern "C" int ls_qc_live_rows(const ls_code *code) { return code ? live_rows(co
 
 // kernel kind: 0 fp32 min-sum, 1 fp16x2 min-sum, 2 sum-product
 static int qc_kind(int variant, int flags) {
-  return variant == LS_SUM_PRODUCT ? 2 : ((flags & LS_QC_FP16) ? 1 : 0);
+  if (variant == LS_SUM_PRODUCT) return (flags & LS_QC_FULL32) ? 3 : 2;
+  return (flags & LS_QC_FP16) ? 1 : 0;
 }
 
 extern "C" int ls_qc_has_kernel(const ls_code *code, int flags) {
   if (!code) return 0;
   const int R = (flags & LS_QC_PRUNE) ? live_rows(code->p) : code->p.mb;
-  const int prec = (flags & LS_QC_SP) ? 2 : qc_kind(LS_MIN_SUM, flags);
-  if (flags & (LS_QC_EXACT | LS_QC_FULL32)) return find_qcx(code) != nullptr;
+  const int prec = (flags & LS_QC_SP) ? qc_kind(LS_SUM_PRODUCT, flags) : qc_kind(LS_MIN_SUM, flags);
+  if ((flags & LS_QC_EXACT) || ((flags & LS_QC_FULL32) && !(flags & LS_QC_SP))) return find_qcx(code) != nullptr;
   if (!code->std_shifts) return 0;
   for (const QcKernelEntry &k : kQcKernels)
     if (k.bg == code->p.bg && k.z == code->p.z && k.r == R && k.prec == prec) return 1;
@@ -322,7 +324,7 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
   const QcParams &P = code->p;
   const float alpha = variant == LS_SCALED_MIN_SUM ? (float)scale : 1.0f;
   cudaStream_t s = as_stream(stream);
-  if (flags & (LS_QC_EXACT | LS_QC_FULL32)) {
+  if ((flags & LS_QC_EXACT) || ((flags & LS_QC_FULL32) && variant != LS_SUM_PRODUCT)) {
     if (variant == LS_SUM_PRODUCT)
       return fail(LS_EINVAL, "ls_qc_decode: the on-chip exact / fp32 full-graph decoder serves min-sum and "
                              "scaled-min-sum; use ls_bp_decode for sum-product");
@@ -343,6 +345,9 @@ extern "C" int ls_qc_decode(const ls_code *code, const float *llr, int64_t batch
         return k.fn(CP, llr, batch, num_iter, alpha, early_stop, hard_k, llr_out, iters_used, ref_bits, counts, s);
     }
   }
+  if (prec == 3)
+    return fail(LS_EINVAL, "ls_qc_decode: no f32 sum-product instance for this (BG, Z, rows); its messages fit "
+                           "in shared memory up to Z = 192 with the dead rows pruned");
   if (prec >= 1) {  // fp16x2 / sum-product at any (Z, R): runtime-geometry instance
     const QcRtEntry *k = prec == 1 ? pick_rt(kQcRtKernels, P.bg, P.z, R) : pick_rt(kQcSpRtKernels, P.bg, P.z, R);
     if (!k)

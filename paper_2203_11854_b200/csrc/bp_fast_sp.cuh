@@ -294,6 +294,256 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// f32-message sum-product (k_qc_sp32): the accuracy option.  Messages and
+// posteriors are f32 (in base-2 units), the check update runs in the LOG
+// domain like the reference (ldpc.py:139-143) but without its cancellation:
+// phi of every edge (ex2 + rcp + lg2, Taylor for 1 - 2^-y near 0), the
+// exclusive sums from prefix and suffix sums (no S - phi_e subtraction),
+// phi of each exclusive sum, clipped as the reference clips.  The first
+// iteration reproduces the reference's float32 pass (ldpc.py:118-122: f32
+// input keeps v2c and phi in f32, where tanh saturates): phi from f32 tanh
+// and log, the check sum in numpy's pairwise order and S - phi_e in f32.
+// Later iterations are f64 in the reference; f32 with the prefix/suffix sums
+// tracks them to ~1e-6 relative.  6 MUFU per edge (fp16 kernel: 4); shared
+// memory 4 * (NE + NCOL) * Z bytes, so it serves codes up to Z = 192 (config
+// 3, dead rows pruned) and the small BG2 codes.
+constexpr float kMsgClip2 = 30.0f * kLog2e;
+
+// phi in base 2 for y clipped to the reference's [1e-12, 40] (natural
+// units).  For u = 2^-y < 1/4 (reliable edges) phi = (2/ln2) atanh(u) as its
+// odd series to u^11 (truncation < 3e-8 relative): lg2.approx carries an
+// ABSOLUTE error near 2^-22, which would swamp the small phi of a reliable
+// edge; above it the ratio's lg2 is far from 0 and accurate.
+__device__ __forceinline__ float sp32_phi2(float y) {
+  y = fminf(fmaxf(y, kPhiLo2), kClip2);
+  const float u = ex2_ftz(-y);
+  const float w = u * u;
+  const float series =
+      u * fmaf(w, fmaf(w, fmaf(w, fmaf(w, fmaf(w, 1.0f / 11.0f, 1.0f / 9.0f), 1.0f / 7.0f), 1.0f / 5.0f), 1.0f / 3.0f),
+               1.0f) * (2.0f * kLog2e);
+  const float logr = lg2_ftz((1.0f + u) * rcp_ftz(sp_one_minus(y, u)));
+  // branch-free pick (as a branch it diverges at every edge)
+  float r;
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %3, 0f3E800000;\n\tselp.f32 %0, %1, %2, p;\n\t}"
+      : "=f"(r) : "f"(series), "f"(logr), "f"(u));
+  return r;
+}
+
+// the reference's float32 phi of iteration 1 (natural units in, base 2 out):
+// f32 tanh and log as numpy evaluates them (tanh saturates near 18).  Not
+// inlined: it runs in the first iteration only, and inlining the library
+// tanhf / logf at every edge of the unrolled graph would multiply the code
+// size (and the instruction-cache misses of the 19 other iterations)
+static __device__ __noinline__ float sp32_phi_first(float y2) {
+  const float x = fminf(fmaxf(y2 * kLn2, 1e-12f), 40.0f);
+  return -logf(tanhf(0.5f * x)) * kLog2e;
+}
+
+template <int N>
+__device__ __forceinline__ float sp32_pairwise(const float *x) {  // numpy pairwise_sum, f32
+  if constexpr (N < 8) {
+    float r = -0.0f;
+#pragma unroll
+    for (int q = 0; q < N; ++q) r = __fadd_rn(r, x[q]);
+    return r;
+  } else {
+    float r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = x[q];
+    constexpr int NB8 = N - N % 8;
+#pragma unroll
+    for (int q = 8; q < NB8; q += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = __fadd_rn(r[u], x[q + u]);
+    float res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+    for (int q = NB8; q < N; ++q) res = __fadd_rn(res, x[q]);
+    return res;
+  }
+}
+
+template <class Geo, bool ES>
+__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
+    k_qc_sp32(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int num_iter,
+              uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
+              const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts) {
+  using G = typename Geo::G;
+  constexpr int SPLIT = Geo::SPLIT;
+  const int Z = geo.z(), NT = geo.nt(), NCOLZ = geo.ncol() * Z;
+  extern __shared__ float smf[];
+  float *c2v = smf;                         // [NE][Z]
+  float *tot = smf + (size_t)geo.ne() * Z;  // [NCOL][Z]
+  char *const totb = reinterpret_cast<char *>(tot);
+  const int t = threadIdx.x;
+  const int h = t / geo.nt1();
+  const int i = t - h * geo.nt1();
+  const bool lane = geo.full_lanes() || i < Z;
+  const int64_t b = blockIdx.x;
+  const float *row = llr + b * (int64_t)P.n;
+
+  for (int v = t; v < NCOLZ; v += NT) tot[v] = chan_value(P, row, v) * kLog2e;
+  for (int q = t; q < geo.ne() * Z; q += NT) c2v[q] = 0.0f;
+  __syncthreads();
+
+  // one check-node phase; FIRST = the reference's float32 first pass
+  auto cn_phase = [&](auto first_c) -> uint32_t {
+    constexpr bool first = decltype(first_c)::value;
+    uint32_t synx = 0;
+    if (lane) {
+      sfor<0, SPLIT>([&](auto hc) {
+        constexpr int H = decltype(hc)::value;
+        if (h != H) return;
+        const unsigned i2 = 2u * (tid_volatile() - H * geo.nt1());
+        const int il = (int)(i2 >> 1);
+        sfor<0, (Geo::RB + SPLIT - 1) / SPLIT>([&](auto jc) {
+          constexpr int r = decltype(jc)::value * SPLIT + H;
+          if constexpr (r < Geo::RB) {
+            if (!geo.template live<r>()) return;
+            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
+            float ph[d];
+            uint32_t sg = 0, hs = 0;
+            sfor<e0, e1>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              constexpr int p = e - e0;
+              // the 2-byte-element offsets of the fp16 geometry, doubled
+              const float tv = *reinterpret_cast<const float *>(totb + 2u * geo.template off<e>(i2));
+              if constexpr (ES) hs ^= __float_as_uint(tv);
+              const float x = tv - c2v[geo.template ez<e>() + il];
+              sg |= (__float_as_uint(x) >> 31) << p;
+              if constexpr (first)
+                ph[p] = sp32_phi_first(fabsf(x));
+              else
+                ph[p] = sp32_phi2(fabsf(x));
+            });
+            const uint32_t par = __popc(sg) & 1u;
+            float ex[d];
+            if constexpr (first) {  // the reference's f32 pass: psum in pairwise order, then psum - pmag
+              const float ps = __fadd_rn(ph[0], sp32_pairwise<d - 1>(ph + 1));
+#pragma unroll
+              for (int p = 0; p < d; ++p) ex[p] = __fsub_rn(ps, ph[p]);
+            } else {  // exclusive sums without cancellation: prefix + suffix
+              float acc = 0.0f;
+#pragma unroll
+              for (int p = 0; p < d; ++p) {
+                ex[p] = acc;
+                acc += ph[p];
+              }
+              acc = 0.0f;
+#pragma unroll
+              for (int p = d - 1; p >= 0; --p) {
+                ex[p] += acc;
+                acc += ph[p];
+              }
+            }
+            sfor<e0, e1>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              constexpr int p = e - e0;
+              float m;
+              if constexpr (first)
+                m = sp32_phi_first(ex[p]);
+              else
+                m = sp32_phi2(ex[p]);
+              m = fminf(m, kMsgClip2);
+              const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
+              c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
+            });
+            if constexpr (ES) synx |= hs;
+          }
+        });
+      });
+    }
+    return synx;
+  };
+
+  int used = num_iter;
+  for (int it = 0; it < num_iter; ++it) {
+    const uint32_t synx = it == 0 ? cn_phase(std::true_type{}) : cn_phase(std::false_type{});
+    if (ES && it > 0) {
+      if (!__syncthreads_or(lane && (synx >> 31))) {
+        used = it;
+        break;
+      }
+    } else {
+      __syncthreads();
+    }
+    if (lane) {
+      sfor<0, SPLIT>([&](auto hc) {
+        constexpr int H = decltype(hc)::value;
+        if (h != H) return;
+        const int j = (int)tid_volatile() - H * geo.nt1();
+        sfor<0, (Geo::NCOL_MAX + SPLIT - 1) / SPLIT>([&](auto cc) {
+          constexpr int c = decltype(cc)::value * SPLIT + H;
+          if constexpr (c < Geo::NCOL_MAX) {
+            if (c >= geo.ncol()) return;
+            float sum = chan_value(P, row, c * Z + j) * kLog2e;
+            constexpr int q0 = G::col_start[c], q1 = G::col_start[c + 1];
+            sfor<q0, q1>([&](auto qc) {
+              constexpr int e = G::col_entry[decltype(qc)::value];
+              if constexpr (G::row[e] < Geo::RB) {
+                if (geo.template live<G::row[e]>()) sum += c2v[geo.template src<e>(j)];
+              }
+            });
+            tot[c * Z + j] = fminf(fmaxf(sum, -kClip2), kClip2);
+          }
+        });
+      });
+    }
+    __syncthreads();
+  }
+
+  if (iters_used && t == 0) iters_used[b] = used;
+  if (llr_out) {
+    float *o = llr_out + b * (int64_t)P.n_full;
+    for (int v = t; v < P.n_full; v += NT) o[v] = v < NCOLZ ? -tot[v] * kLn2 : -chan_value(P, row, v);
+  }
+  unsigned err = 0;
+  for (int v = t; v < P.k; v += NT) {
+    const uint8_t hd = (-tot[v]) > 0.0f;
+    if (hard_k) hard_k[b * (int64_t)P.k + v] = hd;
+    if (ref) err += (hd != ref[b * (int64_t)P.k + v]);
+  }
+  if (ref && counts) {
+    __shared__ unsigned red[Geo::NT_MAX / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+    if ((t & 31) == 0) red[t >> 5] = err;
+    __syncthreads();
+    if (t == 0) {
+      unsigned long long tt = 0;
+      for (int w = 0; w < NT / 32; ++w) tt += red[w];
+      if (tt) {
+        atomicAdd(&counts[0], tt);
+        atomicAdd(&counts[1], 1ULL);
+      }
+    }
+  }
+}
+
+template <class G, int Z, int R, int SPLIT>
+int launch_qc_sp32(const QcChanParams &P, const float *llr, int64_t B, int num_iter, float alpha, int early_stop,
+                   uint8_t *hard_k, float *llr_out, int32_t *iters_used, const uint8_t *ref,
+                   unsigned long long *counts, cudaStream_t s) {
+  (void)alpha;
+  using S = QcShapeSP<G, Z, R, SPLIT>;
+  constexpr size_t smem = 2 * S::SMEM;  // f32 messages and posteriors
+  static_assert(smem <= 227 * 1024, "f32 sum-product messages do not fit in shared memory");
+  using Geo = SpGeoCT<G, Z, R, SPLIT>;
+  auto kern = early_stop ? k_qc_sp32<Geo, true> : k_qc_sp32<Geo, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
+    const int64_t nb = B - b0 < 0x7fffffff ? B - b0 : 0x7fffffff;
+    kern<<<(unsigned)nb, S::NT, smem, s>>>(P, Geo{}, llr + b0 * P.n, num_iter,
+                                            hard_k ? hard_k + b0 * P.k : nullptr,
+                                            llr_out ? llr_out + b0 * P.n_full : nullptr,
+                                            iters_used ? iters_used + b0 : nullptr,
+                                            ref ? ref + b0 * P.k : nullptr, counts);
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
+}
+
 template <class Geo>
 int launch_sp(const Geo &geo, int nt, size_t smem, const QcChanParams &P, const float *llr, int64_t B,
               int num_iter, int early_stop, uint8_t *hard_k, float *llr_out, int32_t *iters_used,

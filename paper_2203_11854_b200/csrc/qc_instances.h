@@ -10,7 +10,9 @@
 //   1,Z,24 / 2,Z,22 for Z in 32..384 : config 5 decoder-only sweep (BG1 rate
 //                         1/2 and BG2 rate 1/3 lifted at any Z, fp16x2)
 // kind f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh);
-// sp: k_qc_sp, sum-product (bp_fast_sp.cuh)
+// sp: k_qc_sp, sum-product (bp_fast_sp.cuh); sp32: k_qc_sp32, sum-product with
+// f32 messages and the log-domain check update (accuracy option, where the
+// messages fit in shared memory)
 #pragma once
 #define LSB_QC_INSTANCES(X) \
   X(1, 384, 24, 2, f32)     \
@@ -42,7 +44,10 @@
   X(1, 192, 45, 2, sp)      \
   X(1, 192, 46, 2, sp)      \
   X(2, 26, 12, 1, sp)       \
-  X(2, 26, 42, 1, sp)
+  X(2, 26, 42, 1, sp)       \
+  X(1, 192, 24, 2, sp32)    \
+  X(2, 26, 12, 1, sp32)     \
+  X(2, 26, 42, 1, sp32)
 
 // Runtime-geometry fp16x2 instances (base graph, row bound RB, threads per
 // lane): any Z <= 384 (<= 192 with 4 threads per lane) and any processed-row

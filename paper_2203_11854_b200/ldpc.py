@@ -309,8 +309,11 @@ def qc_has_kernel(code: LdpcCode5G, precision: str = "fp32", prune: bool = True,
     (the sum-product fast decoder exists only as such instances; min-sum codes
     without one run the runtime-geometry fp16x2 or the runtime-Z fp32 kernel).
     precision "exact" asks for the on-chip exact decoder (min-sum variants)."""
-    if precision in ("exact", "fp32-full"):
+    if precision == "exact":
         return variant != "sum-product" and bool(L.lib().ls_qc_has_kernel(code.handle, LS_QC_EXACT))
+    if precision == "fp32-full":
+        sp = LS_QC_SP | (LS_QC_PRUNE if prune else 0) if variant == "sum-product" else 0
+        return bool(L.lib().ls_qc_has_kernel(code.handle, LS_QC_FULL32 | sp))
     flags = (LS_QC_PRUNE if prune else 0) | (LS_QC_FP16 if precision == "fp16x2" else 0)
     if variant == "sum-product":
         flags |= LS_QC_SP
@@ -338,10 +341,11 @@ def qc_decode(llr, code: LdpcCode5G, num_iter: int = 20, variant: str = "min-sum
         raise ValueError(f"unknown decoder precision {precision!r}")
     if mother and precision not in ("exact", "fp32-full"):
         raise ValueError("mother-length input needs precision='exact' or 'fp32-full'")
-    if precision in ("exact", "fp32-full"):
+    if precision == "exact" or (precision == "fp32-full" and variant != "sum-product"):
         prune = False
     elif prune is None:
-        prune = not want_llr
+        # f32 sum-product messages fit in shared memory only with the dead rows pruned
+        prune = (not want_llr) or (precision == "fp32-full" and variant == "sum-product")
     flags = ((LS_QC_PRUNE if prune else 0) | (LS_QC_GENERIC if generic else 0)
              | (LS_QC_FP16 if precision == "fp16x2" else 0) | (LS_QC_EXACT if precision == "exact" else 0)
              | (LS_QC_FULL32 if precision == "fp32-full" else 0) | (LS_QC_MOTHER if mother else 0))

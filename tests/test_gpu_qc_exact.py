@@ -198,3 +198,40 @@ def test_fp32_full_graph_noiseless_and_fixed_iterations():
                          want_iters=True)
         assert np.array_equal(r["hard"].cpu().numpy(), bits)
         assert r["counts"].tolist() == [0, 0]
+
+
+@pytest.mark.parametrize("k,n,m,ebno", [(4096, 8192, 2, 1.75), (4096, 8192, 2, 2.25), (256, 512, 2, 2.0),
+                                        (256, 512, 2, 3.0)])
+def test_sum_product_f32_messages_close_to_exact(k, n, m, ebno):
+    """The f32-message sum-product option (k_qc_sp32: log-domain check update
+    with prefix/suffix exclusive sums, the reference's f32 first pass) against
+    the exact sum-product decoder (CSR engine, the reference's arithmetic): on
+    the codewords both converge on at the same iteration, identical hard
+    decisions and >= 99.9 % of the mother LLRs within 1e-4 * max(|L|, 1) (the
+    SURVEY.md 8c sum-product tier), the rest within 1e-3."""
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    assert LD.qc_has_kernel(code, precision="fp32-full", variant="sum-product")
+    B = 192 if k > 1000 else 400
+    _, llr = _llrs(k, n, m, ebno, B, 44)
+    mother = oc.derate_match(llr)
+    lo_e, hard_e, it_e = lb.bp_decode(mother, code.pcm, 20, "sum-product", 0.75, True, return_iters=True,
+                                      engine="csr")
+    r = LD.qc_decode(llr, code, 20, "sum-product", early_stop=True, want_llr=True, want_iters=True,
+                     precision="fp32-full")
+    R = lb.ldpc.L.lib().ls_qc_live_rows(code.handle)
+    ncol = code._kb + max(R, 4)  # the pruned dead rows' parity posteriors are channel values
+    it_f = r["iters"].cpu().numpy()
+    conv = (it_e < 20) & (it_e == it_f)
+    assert conv.sum() >= B // 4
+    le, lf = lo_e[conv][:, : ncol * code.z], r["llr"].cpu().numpy()[conv][:, : ncol * code.z]
+    d = np.abs(le - lf) / np.maximum(np.abs(le), 1.0)
+    assert (d <= 1e-4).mean() >= 0.999 and d.max() <= 1e-3
+    assert np.array_equal(r["hard"].cpu().numpy()[conv], hard_e[conv][:, :k])
+
+
+def test_sum_product_f32_messages_unavailable_where_they_do_not_fit():
+    code = lb.LdpcCode5G(8448, 16896)
+    assert not LD.qc_has_kernel(code, precision="fp32-full", variant="sum-product")
+    with pytest.raises(ValueError):
+        LD.qc_decode(np.zeros((2, code.n), np.float32), code, 5, "sum-product", precision="fp32-full")
