@@ -443,6 +443,9 @@ def fast_rate(a, rank, world, dist, precision, prune, steps=3):
             "kernel": {"fp16x2": "k_qc_fast_h2w", "fp32-full": "k_qc_exact<BG1,384,2,float>"}.get(precision, precision),
             "rows": "24 live rows (dead extension rows pruned)" if prune else "all 46 rows",
             "roofline_frac": B * _bytes_cw(a.iters) / (dms / 1e3) / 1e9 / float(_peaks().get("hbm_gbs", 6650.0)),
+            # DRAM bytes per launch at B=65,536 from ncu --set full (profiles/r02/ncu_*_bench_summary.txt)
+            "traffic_per_launch_at_65536": {"fp16x2": 4_992_890_000 + 5_429_504,
+                                            "fp32-full": 5_013_454_000 + 9_787_904}.get(precision),
             "bit_errors": c[0], "block_errors": c[1], "clocks": clk,
             "note": "fast mode: Philox noise, f32 modem, narrower message arithmetic; statistically "
                     "equivalent to the reference, not bit-exact"}
