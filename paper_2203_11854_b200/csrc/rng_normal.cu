@@ -24,6 +24,7 @@
 // the tables with its own random level, which the constant cache serialises
 #define LS_ZIG_QUAL static __device__ const
 #include "common.cuh"
+#include "glibc_exp_table.h"
 #include "ziggurat_tables.h"
 
 namespace lsb {
@@ -110,6 +111,25 @@ __device__ double glibc_log1p(double x) {
   return fma(dk, ln2_hi, -((hfsq - (fma(dk, ln2_lo, c) + (hfsq + R) * s)) - f));
 }
 
+// exp(x) as the x86-64 glibc 2.39 libm numpy's ziggurat calls computes it,
+// to the bit, for |x| < 512 (the wedge test's -x^2/2 lies in [-6.68, 0]):
+// x = k ln2/128 + r, 2^(k/128) from glibc's table (tools/gen_glibc_exp_header.py),
+// exp(r) by its degree-5 polynomial, with the fused multiply-adds of glibc's
+// FMA build (checked against the host libm on 2e7 arguments in [-7, 0]).
+__device__ __forceinline__ double glibc_exp(double x) {
+  double kd = fma(LS_GEXP_INVLN2N, x, LS_GEXP_SHIFT);
+  const uint64_t ki = (uint64_t)__double_as_longlong(kd);
+  kd -= LS_GEXP_SHIFT;
+  const double r = fma(kd, LS_GEXP_NEGLN2LON, fma(kd, LS_GEXP_NEGLN2HIN, x));
+  const uint64_t idx = 2 * (ki % 128);
+  const double tail = __longlong_as_double((long long)ls_gexp_tab[idx]);
+  const uint64_t sbits = ls_gexp_tab[idx + 1] + (ki << (52 - 7));
+  const double r2 = r * r;
+  const double tmp = fma(r2 * r2, fma(r, LS_GEXP_C5, LS_GEXP_C4), fma(r2, fma(r, LS_GEXP_C3, LS_GEXP_C2), tail + r));
+  const double scale = __longlong_as_double((long long)sbits);
+  return fma(scale, tmp, scale);
+}
+
 // draw starting at word p: value and number of words consumed
 __device__ double zig_draw(uint64_t seed, uint64_t sid, int64_t p, int *len) {
   const int64_t p0 = p;
@@ -136,7 +156,7 @@ __device__ double zig_draw(uint64_t seed, uint64_t sid, int64_t p, int *len) {
       }
     } else {
       const double u = dbl_at(seed, sid, p++);
-      if (((ls_zig_fi[idx - 1] - ls_zig_fi[idx]) * u + ls_zig_fi[idx]) < exp(-0.5 * x * x)) {
+      if (((ls_zig_fi[idx - 1] - ls_zig_fi[idx]) * u + ls_zig_fi[idx]) < glibc_exp(-0.5 * x * x)) {
         *len = (int)(p - p0);
         return x;
       }

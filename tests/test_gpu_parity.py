@@ -868,3 +868,13 @@ def test_persistent_early_stop_slot_refill_is_deterministic(ebno, monkeypatch):
     for _ in range(12):
         got = run()
         assert all(np.array_equal(x, y) for x, y in zip(got, ref))
+
+
+def test_standard_normal_bit_exact_20m_draws():
+    """20 M draws on two keys equal numpy's: ~140 k of them take the wedge
+    test, whose exp is the glibc replica (csrc/rng_normal.cu: glibc_exp), and
+    ~2 k the tail (glibc log1p replica)."""
+    for seed, sid in ((2024, 77), (99, (7 << 32) | 3)):
+        got = lb.channel.standard_normal(10_000_000, lb.RngStream(seed, sid))
+        ref = lb.RngStream(seed, sid).generator().standard_normal(10_000_000)
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
