@@ -18,9 +18,9 @@
 // Data layout for one codeword per CTA (persistent, one CTA per SM at
 // Z = 384):
 //   shared  M1 [MB][Z] f64     alpha*min1 of every check
-//           W  [MB][Z] u16/u32 argmin << deg | outgoing signs, position p
-//                              at bit deg-1-p (u32 only for rows whose
-//                              deg + log2(deg) > 16)
+//           W  [MB][Z] u16/u32 outgoing signs (position p at bit deg-1-p)
+//                              | argmin, one-hot at bit deg + p for rows of
+//                              degree <= 16, else the position << deg
 //           T  [KBC][Z] f32    posteriors of the core columns (systematic +
 //                              4 core parity; KBC = k_b + 4)
 //   global  m2 [MB][Z] f64     alpha*min2 per check, one slice per CTA: read
@@ -77,7 +77,14 @@ struct QxGeo {
     while ((1 << b) < d) ++b;
     return b;
   }
-  static constexpr int wbytes(int r) { return deg(r) + argbits(deg(r)) <= 16 ? 2 : 4; }
+  // argmin as a one-hot field (bit deg + p) when 2 deg <= 32 -- one bit test
+  // per edge instead of an extract and compare -- else as an index (<< deg)
+  static constexpr bool onehot(int r) { return 2 * deg(r) <= 32; }
+  static constexpr int wbits(int r) { return onehot(r) ? 2 * deg(r) : deg(r) + argbits(deg(r)); }
+  static constexpr int wbytes(int r) { return wbits(r) <= 16 ? 2 : 4; }
+  static constexpr uint32_t argcode(int r, int p) {
+    return onehot(r) ? (1u << (deg(r) + p)) : ((uint32_t)p << deg(r));
+  }
   // shared: M1 [MB][Z] M, (fp32: M2 [MB][Z] M), W, T
   static constexpr int M2_OFF = (int)sizeof(M_) * MB * Z;
   static constexpr int W_OFF = EXACT ? M2_OFF : 2 * M2_OFF;
@@ -128,6 +135,16 @@ struct QxGeo {
     return g;
   }
 };
+
+// is position p of row r the argmin of the check whose word is w
+template <class Geo, int r, int p>
+__device__ __forceinline__ bool qx_isarg(uint32_t w) {
+  constexpr int D = Geo::deg(r);
+  if constexpr (Geo::onehot(r))
+    return (w & (1u << (D + p))) != 0u;
+  else
+    return (w >> D) == (uint32_t)p;
+}
 
 // x with its sign bit flipped when `bit31` is 0x80000000 (c2v = (-alpha)*excl)
 __device__ __forceinline__ double qx_flip(double x, uint32_t bit31) {
@@ -198,7 +215,7 @@ __device__ __forceinline__ void qx_vn_gather(typename Geo::M *x, uint32_t j8, co
     const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
     const uint32_t oM = SZ == 8 ? o8 : (o8 >> 1);  // byte offset of check (r, i) in an [MB][Z] M array
     M mag;
-    if ((w >> D) == (uint32_t)p) {
+    if (qx_isarg<Geo, r, p>(w)) {
       if constexpr (Geo::EXACT)
         mag = *reinterpret_cast<const M *>(reinterpret_cast<const char *>(m2) + SZ * r * Z + oM);
       else
@@ -285,14 +302,13 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             m2o = m2[ci];
             wo = (uint32_t)W[ln];
           }
-          const uint32_t argo = wo >> D;
           M mn1 = (M)INFINITY, mn2 = (M)INFINITY;
           uint32_t arg = 0, sg = 0, syn = 0;
           sfor<0, D>([&](auto pc) {
             constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
             // old message on this edge: +-(alpha*min1 | alpha*min2), sign
             // bit of position p at bit D-1-p of the word
-            const M mag = argo == (uint32_t)p ? m2o : m1o;
+            const M mag = qx_isarg<Geo, r, p>(wo) ? m2o : m1o;
             const M cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
             uint32_t o = i4 + 4u * s;  // byte offset of lane (i + s) mod Z
             o = min(o, o - 4u * Z);
@@ -314,10 +330,10 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
               const double t2 = lt2 ? a : mn2;
               mn2 = lt1 ? mn1 : t2;
               mn1 = lt1 ? a : mn1;
-              arg = lt1 ? (uint32_t)p : arg;
+              arg = lt1 ? Geo::argcode(r, p) : arg;
             } else {  // one FMNMX per update in f32
               const float a = fabsf(x);
-              arg = a < mn1 ? (uint32_t)p : arg;
+              arg = a < mn1 ? Geo::argcode(r, p) : arg;
               mn2 = fminf(mn2, fmaxf(mn1, a));
               mn1 = fminf(mn1, a);
             }
@@ -327,7 +343,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
           M1[ci] = qx_mul(al, mn1);
           m2[ci] = qx_mul(al, mn2);
-          W[ln] = (WT)(osg | (arg << D));
+          W[ln] = (WT)(osg | arg);
         });
       }
       if (ES && !first) {
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
             const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
             const uint32_t w = W[i];
-            const M mag = (w >> D) == (uint32_t)(D - 1) ? m2[r * Z + i] : M1[r * Z + i];
+            const M mag = qx_isarg<Geo, r, D - 1>(w) ? m2[r * Z + i] : M1[r * Z + i];
             const M cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
             int j = i + s;
             j = j >= Z ? j - Z : j;
