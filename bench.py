@@ -610,8 +610,8 @@ def sum_product_f32_rate(a, B=32768):
         ms = e0.elapsed_time(e1)
         out["f32_messages" if prec == "fp32-full" else "fp16_messages"] = {
             "ms": ms, "gbit_s": B * 4096 / (ms / 1e3) / 1e9}
-    out["note"] = ("decoder only, 20 fixed iterations, 2.0 dB; f32 messages: k_qc_sp32 (6 MUFU per edge, "
-                   "log domain, prefix/suffix exclusive sums); fp16 messages: k_qc_sp (4 MUFU, product domain)")
+    out["note"] = ("decoder only, 20 fixed iterations, 2.0 dB; f32 messages: k_qc_sp32 (3 MUFU per edge, "
+                   "division-free product domain with prefix/suffix products); fp16 messages: k_qc_sp (4 MUFU, product domain)")
     return out
 
 

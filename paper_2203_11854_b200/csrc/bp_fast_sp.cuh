@@ -296,39 +296,17 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
 
 // ---------------------------------------------------------------------------
 // f32-message sum-product (k_qc_sp32): the accuracy option.  Messages and
-// posteriors are f32 (in base-2 units), the check update runs in the LOG
-// domain like the reference (ldpc.py:139-143) but without its cancellation:
-// phi of every edge (ex2 + rcp + lg2, Taylor for 1 - 2^-y near 0), the
-// exclusive sums from prefix and suffix sums (no S - phi_e subtraction),
-// phi of each exclusive sum, clipped as the reference clips.  The first
-// iteration reproduces the reference's float32 pass (ldpc.py:118-122: f32
-// input keeps v2c and phi in f32, where tanh saturates): phi from f32 tanh
-// and log, the check sum in numpy's pairwise order and S - phi_e in f32.
-// Later iterations are f64 in the reference; f32 with the prefix/suffix sums
-// tracks them to ~1e-6 relative.  6 MUFU per edge (fp16 kernel: 4); shared
-// memory 4 * (NE + NCOL) * Z bytes, so it serves codes up to Z = 192 (config
-// 3, dead rows pruned) and the small BG2 codes.
+// posteriors are f32 (in base-2 units).  The first iteration reproduces the
+// reference's float32 pass (ldpc.py:118-122: f32 input keeps v2c and phi in
+// f32, where tanh saturates): phi from f32 tanh and log, the check sum in
+// numpy's pairwise order and S - phi_e in f32.  Later iterations are f64 in
+// the reference (ldpc.py:139-143); here they run in the product domain
+// (sp32_msg below) with prefix/suffix products for the exclusive sets, which
+// tracks the f64 log-domain result to ~1e-6 relative without its S - phi_e
+// cancellation.  3 MUFU per edge; shared memory 4 * (NE + NCOL) * Z bytes, so
+// it serves codes up to Z = 192 (config 3, dead rows pruned) and the small
+// BG2 codes.
 constexpr float kMsgClip2 = 30.0f * kLog2e;
-
-// phi in base 2 for y clipped to the reference's [1e-12, 40] (natural
-// units).  For u = 2^-y < 1/4 (reliable edges) phi = (2/ln2) atanh(u) as its
-// odd series to u^11 (truncation < 3e-8 relative): lg2.approx carries an
-// ABSOLUTE error near 2^-22, which would swamp the small phi of a reliable
-// edge; above it the ratio's lg2 is far from 0 and accurate.
-__device__ __forceinline__ float sp32_phi2(float y) {
-  y = fminf(fmaxf(y, kPhiLo2), kClip2);
-  const float u = ex2_ftz(-y);
-  const float w = u * u;
-  const float series =
-      u * fmaf(w, fmaf(w, fmaf(w, fmaf(w, fmaf(w, 1.0f / 11.0f, 1.0f / 9.0f), 1.0f / 7.0f), 1.0f / 5.0f), 1.0f / 3.0f),
-               1.0f) * (2.0f * kLog2e);
-  const float logr = lg2_ftz((1.0f + u) * rcp_ftz(sp_one_minus(y, u)));
-  // branch-free pick (as a branch it diverges at every edge)
-  float r;
-  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %3, 0f3E800000;\n\tselp.f32 %0, %1, %2, p;\n\t}"
-      : "=f"(r) : "f"(series), "f"(logr), "f"(u));
-  return r;
-}
 
 // the reference's float32 phi of iteration 1 (natural units in, base 2 out):
 // f32 tanh and log as numpy evaluates them (tanh saturates near 18).  Not
@@ -338,6 +316,28 @@ __device__ __forceinline__ float sp32_phi2(float y) {
 static __device__ __noinline__ float sp32_phi_first(float y2) {
   const float x = fminf(fmaxf(y2 * kLn2, 1e-12f), 40.0f);
   return -logf(tanhf(0.5f * x)) * kLog2e;
+}
+
+// Later iterations work in the product domain without a division or a
+// cancellation: over a set of edges with u_e = 2^-y_e, N = prod (1 - u_e),
+// Q = prod (1 + u_e) and P = Q - N (accumulated as P (1 + u) + 2 u N, all
+// terms positive).  The log-domain sum of phi is ln(Q / N), and phi of it is
+// ln((Q + N) / (Q - N)) = ln(1 + z), z = 2 N / P -- one ex2 per edge on the
+// way in and one rcp + lg2 on the way out (3 MUFU per edge, the log-domain
+// form needs 6).  The reference's clip of the exclusive sum to [1e-12, 40]
+// (natural units) is z in [2 / (e^40 - 1), 2e12]; the message clip at 30
+// never binds below that (lg2(1 + 2e12) = 28.3 nats).  lg2.approx has an
+// absolute error near 2^-22, so small z takes the log1p series instead.
+constexpr float kZMax = 2e12f, kZMin = 8.5e-18f;
+__device__ __forceinline__ float sp32_msg(float n_ex, float p_ex) {
+  const float z = fminf(fmaxf(2.0f * n_ex * rcp_ftz(p_ex), kZMin), kZMax);
+  const float series =
+      z * fmaf(z, fmaf(z, fmaf(z, fmaf(z, 0.2f * kLog2e, -0.25f * kLog2e), kLog2e / 3.0f), -0.5f * kLog2e), kLog2e);
+  const float lg = lg2_ftz(1.0f + z);
+  float r;
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %3, 0f3C800000;\n\tselp.f32 %0, %1, %2, p;\n\t}"
+      : "=f"(r) : "f"(series), "f"(lg), "f"(z));
+  return r;
 }
 
 template <int N>
@@ -401,7 +401,10 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
           if constexpr (r < Geo::RB) {
             if (!geo.template live<r>()) return;
             constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            float ph[d];
+            // first pass: phi per edge; later: u = 2^-y, n = 1 - u per edge and
+            // the prefix products (pn, pp) = (N, P) of the edges before it
+            float ph[first ? d : 1], uu[first ? 1 : d], nn[first ? 1 : d], pn[first ? 1 : d], pp[first ? 1 : d];
+            float na = 1.0f, pa = 0.0f;
             uint32_t sg = 0, hs = 0;
             sfor<e0, e1>([&](auto ec) {
               constexpr int e = decltype(ec)::value;
@@ -411,43 +414,43 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
               if constexpr (ES) hs ^= __float_as_uint(tv);
               const float x = tv - c2v[geo.template ez<e>() + il];
               sg |= (__float_as_uint(x) >> 31) << p;
-              if constexpr (first)
+              if constexpr (first) {
                 ph[p] = sp32_phi_first(fabsf(x));
-              else
-                ph[p] = sp32_phi2(fabsf(x));
+              } else {
+                const float y = fminf(fmaxf(fabsf(x), kPhiLo2), kClip2);
+                const float u = ex2_ftz(-y);
+                uu[p] = u;
+                nn[p] = sp_one_minus(y, u);
+                pn[p] = na;
+                pp[p] = pa;
+                // (N, P) <- (N (1 - u), P (1 + u) + 2 u N): Q = N + P stays implicit
+                pa = fmaf(2.0f * u, na, fmaf(pa, u, pa));
+                na *= nn[p];
+              }
             });
             const uint32_t par = __popc(sg) & 1u;
-            float ex[d];
             if constexpr (first) {  // the reference's f32 pass: psum in pairwise order, then psum - pmag
               const float ps = __fadd_rn(ph[0], sp32_pairwise<d - 1>(ph + 1));
-#pragma unroll
-              for (int p = 0; p < d; ++p) ex[p] = __fsub_rn(ps, ph[p]);
-            } else {  // exclusive sums without cancellation: prefix + suffix
-              float acc = 0.0f;
-#pragma unroll
-              for (int p = 0; p < d; ++p) {
-                ex[p] = acc;
-                acc += ph[p];
-              }
-              acc = 0.0f;
-#pragma unroll
-              for (int p = d - 1; p >= 0; --p) {
-                ex[p] += acc;
-                acc += ph[p];
-              }
+              sfor<e0, e1>([&](auto ec) {
+                constexpr int e = decltype(ec)::value;
+                constexpr int p = e - e0;
+                const float m = fminf(sp32_phi_first(__fsub_rn(ps, ph[p])), kMsgClip2);
+                const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
+                c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
+              });
+            } else {
+              // exclusive (N, P) of every edge from the prefix (pn, pp) and a
+              // running suffix (nb, pb): N_ex = N_a N_b, P_ex = P_a Q_b + N_a P_b
+              float nb = 1.0f, pb = 0.0f;
+              sfor<0, d>([&](auto qc) {
+                constexpr int p = d - 1 - decltype(qc)::value, e = e0 + p;
+                const float m = sp32_msg(pn[p] * nb, fmaf(pp[p], nb + pb, pn[p] * pb));
+                const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
+                c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
+                pb = fmaf(2.0f * uu[p], nb, fmaf(pb, uu[p], pb));
+                nb *= nn[p];
+              });
             }
-            sfor<e0, e1>([&](auto ec) {
-              constexpr int e = decltype(ec)::value;
-              constexpr int p = e - e0;
-              float m;
-              if constexpr (first)
-                m = sp32_phi_first(ex[p]);
-              else
-                m = sp32_phi2(ex[p]);
-              m = fminf(m, kMsgClip2);
-              const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
-              c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
-            });
             if constexpr (ES) synx |= hs;
           }
         });
