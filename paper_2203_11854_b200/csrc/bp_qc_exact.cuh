@@ -59,14 +59,20 @@ namespace lsb {
 
 // M = double: the EXACT decoder (reference arithmetic); M = float: the fp32
 // full-graph fast decoder (same schedule and layout with f32 messages, so
-// min2 fits in shared memory too)
-template <class G_, int Z_, int NTL_, class M_ = double>
+// min2 fits in shared memory too).  NC codewords per CTA (slots) run in
+// lockstep for Z < 384: every row's code then serves NC * Z lanes, as many
+// warps as at Z = 384, and the instruction cache is shared (one codeword of
+// Z = 192 per CTA left half the warps per row and stalled on instruction
+// fetch, profiles/r02/README.md).
+constexpr int qx_default_nc(int z) { return z >= 384 ? 1 : 384 / z; }
+
+template <class G_, int Z_, int NTL_, class M_ = double, int NC_ = qx_default_nc(Z_)>
 struct QxGeo {
   using G = G_;
   using M = M_;
   static constexpr bool EXACT = sizeof(M_) == 8;
-  static constexpr int Z = Z_, NTL = NTL_;
-  static constexpr int NT1 = ((Z + 31) / 32) * 32, NT = NT1 * NTL;
+  static constexpr int Z = Z_, NTL = NTL_, NC = NC_, NZ = NC_ * Z_;
+  static constexpr int NT1 = ((NZ + 31) / 32) * 32, NT = NT1 * NTL;
   static constexpr int MB = G::MB, NB = G::NB, KBC = G::KB + 4, NEXT = G::NB - (G::KB + 4);
   static constexpr int MINB = NT >= 768 ? 1 : (NT >= 384 ? 2 : (NT >= 256 ? 4 : 1024 / NT));
 
@@ -85,20 +91,21 @@ struct QxGeo {
   static constexpr uint32_t argcode(int r, int p) {
     return onehot(r) ? (1u << (deg(r) + p)) : ((uint32_t)p << deg(r));
   }
-  // shared: M1 [MB][Z] M, (fp32: M2 [MB][Z] M), W, T
-  static constexpr int M2_OFF = (int)sizeof(M_) * MB * Z;
+  // shared: M1 [MB][NZ] M, (fp32: M2 [MB][NZ] M), W, T [KBC][NZ]; lane
+  // k * Z + i of a row is lane i of slot k
+  static constexpr int M2_OFF = (int)sizeof(M_) * MB * NZ;
   static constexpr int W_OFF = EXACT ? M2_OFF : 2 * M2_OFF;
   static constexpr int woff(int r) {  // byte offset of row r's word array
     int o = W_OFF;
     for (int q = 0; q < r; ++q) {
       if (wbytes(q) == 4) o = (o + 3) & ~3;
-      o += wbytes(q) * Z;
+      o += wbytes(q) * NZ;
     }
     if (wbytes(r) == 4) o = (o + 3) & ~3;
     return o;
   }
-  static constexpr int T_OFF = (woff(MB - 1) + wbytes(MB - 1) * Z + 15) & ~15;
-  static constexpr int SMEM = T_OFF + 4 * KBC * Z;
+  static constexpr int T_OFF = (woff(MB - 1) + wbytes(MB - 1) * NZ + 15) & ~15;
+  static constexpr int SMEM = T_OFF + 4 * KBC * NZ;
 
   // contiguous degree-balanced ranges: rows [rfirst(g), rfirst(g+1)) and
   // core columns [cfirst(g), cfirst(g+1)) belong to thread group g
@@ -198,30 +205,38 @@ __device__ __forceinline__ float qx_chan(const QcChanParams &P, const float *__r
   return mother ? -__ldg(row + v) : chan_value(P, row, v);
 }
 
-// gather the messages into core column c at lane j (ascending check order):
-// c2v = +-(alpha*min1 | alpha*min2) from the compressed state of each check
+// next codeword of the batch, -1 when it is exhausted
+__device__ __forceinline__ long long qx_claim(unsigned long long *next, int64_t batch) {
+  const unsigned long long c = atomicAdd(next, 1ULL);
+  return (long long)c < batch ? (long long)c : -1;
+}
+
+// gather the messages into core column c at lane j of the slot whose lanes
+// start at byte k8 / 8 * sizeof(M) (ascending check order): c2v =
+// +-(alpha*min1 | alpha*min2) from the compressed state of each check
 template <class Geo, int c>
-__device__ __forceinline__ void qx_vn_gather(typename Geo::M *x, uint32_t j8, const unsigned char *qx_sm,
-                                             const typename Geo::M *m2) {
+__device__ __forceinline__ void qx_vn_gather(typename Geo::M *x, uint32_t j8, uint32_t k8,
+                                             const unsigned char *qx_sm, const typename Geo::M *m2) {
   using G = typename Geo::G;
   using M = typename Geo::M;
-  constexpr int Z = Geo::Z, d = Geo::cdeg(c), cs = G::col_start[c], SZ = (int)sizeof(M);
+  constexpr int Z = Geo::Z, NZ = Geo::NZ, d = Geo::cdeg(c), cs = G::col_start[c], SZ = (int)sizeof(M);
   sfor<0, d>([&](auto tc) {
     constexpr int q = decltype(tc)::value, e = G::col_entry[cs + q], r = G::row[e];
     constexpr int p = e - G::row_start[r], D = Geo::deg(r), s = G::shift[e] % Z;
     using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
     uint32_t o8 = j8 - 8u * s;  // 8 * ((j - s) mod Z)
     o8 = min(o8, o8 + 8u * Z);
+    if constexpr (Geo::NC > 1) o8 += k8;
     const uint32_t w = *reinterpret_cast<const WT *>(qx_sm + Geo::woff(r) + (o8 >> (sizeof(WT) == 4 ? 1 : 2)));
-    const uint32_t oM = SZ == 8 ? o8 : (o8 >> 1);  // byte offset of check (r, i) in an [MB][Z] M array
+    const uint32_t oM = SZ == 8 ? o8 : (o8 >> 1);  // byte offset of check (r, lane) in an [MB][NZ] M array
     M mag;
     if (qx_isarg<Geo, r, p>(w)) {
       if constexpr (Geo::EXACT)
-        mag = *reinterpret_cast<const M *>(reinterpret_cast<const char *>(m2) + SZ * r * Z + oM);
+        mag = *reinterpret_cast<const M *>(reinterpret_cast<const char *>(m2) + SZ * r * NZ + oM);
       else
-        mag = *reinterpret_cast<const M *>(qx_sm + Geo::M2_OFF + SZ * r * Z + oM);
+        mag = *reinterpret_cast<const M *>(qx_sm + Geo::M2_OFF + SZ * r * NZ + oM);
     } else {
-      mag = *reinterpret_cast<const M *>(qx_sm + SZ * r * Z + oM);
+      mag = *reinterpret_cast<const M *>(qx_sm + SZ * r * NZ + oM);
     }
     x[q] = qx_flip(mag, (w << (32 - D + p)) & 0x80000000u);
   });
@@ -244,139 +259,185 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
                typename Geo::M *__restrict__ m2ws, float *__restrict__ extws, float *__restrict__ chws) {
   using G = typename Geo::G;
   using M = typename Geo::M;
-  constexpr int Z = Geo::Z, NT1 = Geo::NT1, NT = Geo::NT, MB = Geo::MB, KBC = Geo::KBC;
+  constexpr int Z = Geo::Z, NZ = Geo::NZ, NC = Geo::NC, NT1 = Geo::NT1, NTL = Geo::NTL, MB = Geo::MB;
+  constexpr int KBC = Geo::KBC, SLOT_T = NTL * Z;  // threads per slot
   extern __shared__ __align__(16) unsigned char qx_sm[];
   M *M1 = reinterpret_cast<M *>(qx_sm);
   // min2 per check: an L2 slice per CTA for f64 messages, shared memory for f32
-  M *m2 = Geo::EXACT ? m2ws + (size_t)blockIdx.x * MB * Z : reinterpret_cast<M *>(qx_sm + Geo::M2_OFF);
+  M *m2 = Geo::EXACT ? m2ws + (size_t)blockIdx.x * MB * NZ : reinterpret_cast<M *>(qx_sm + Geo::M2_OFF);
   const M al = (M)alpha;
   float *T = reinterpret_cast<float *>(qx_sm + Geo::T_OFF);
-  __shared__ long long cur;
-  __shared__ unsigned red[NT / 32];
+  __shared__ long long cur[NC], nxt[NC];
+  __shared__ unsigned errs[NC];
+  __shared__ uint32_t flag[2][NC];  // per-slot syndrome flags, double-buffered by CTA iteration
   const int t = threadIdx.x, grp = t / NT1, ln = t - grp * NT1;
-  const bool lane = ln < Z;
-  float *ext = OUT ? extws + (size_t)blockIdx.x * Geo::NEXT * Z : nullptr;
-  // channel values -derate(llr) of the current codeword, formed once per
+  const bool lane = ln < NZ;
+  const int k = NC == 1 || !lane ? 0 : ln / Z;  // slot
+  const int i = ln - k * Z;         // lane within the slot's codeword
+  const int ts = grp * Z + i;       // thread index within the slot
+  float *ext = OUT ? extws + (size_t)blockIdx.x * Geo::NEXT * NZ : nullptr;
+  // channel values -derate(llr) of the slot's codeword, formed once per
   // codeword (fillers, punctured positions, repetitions) and re-read from L2
-  float *chn = chws + (size_t)blockIdx.x * Geo::NB * Z;
+  float *chn = chws + ((size_t)blockIdx.x * NC + k) * Geo::NB * Z;
   const bool moth = mother != 0;
   const int row_len = moth ? P.n_full : P.n;
+  const uint32_t k4 = 4u * (uint32_t)(k * Z), k8 = 2u * k4;  // byte offsets of the slot's lanes
+  // per-thread bases, so that every row / column offset is an immediate
+  M *const M1l = M1 + ln;
+  M *const m2l = m2 + ln;
+  const float *const chj = chn + i;
+  float *const Tkj = T + k * Z + i;
 
-  for (;;) {
-    if (t == 0) {
-      const unsigned long long c = atomicAdd(next, 1ULL);
-      cur = (long long)c < batch ? (long long)c : -1;
-    }
-    __syncthreads();
-    const long long cw = cur;
-    if (cw < 0) return;
-    const float *row = llr + cw * (int64_t)row_len;
-    for (int v = t; v < Geo::NB * Z; v += NT) {
-      const float ch = qx_chan(P, row, v, moth);
-      chn[v] = ch;
-      if (v < KBC * Z) T[v] = ch;
-    }
-    __syncthreads();
-
-    int used = num_iter;
-    for (int it = 0; it < num_iter; ++it) {
-      const bool first = it == 0;
-      uint32_t bad = 0;
-      // ------------------------------------------------ check-node phase
-      if (lane) {
-        uint32_t i4 = 4u * (uint32_t)ln;
-        // opaque per iteration: keeps the ~600 per-edge lane offsets from
-        // being hoisted out of the iteration loop (and spilled)
-        asm volatile("" : "+r"(i4));
-        sfor<0, MB>([&](auto rc) {
-          constexpr int r = decltype(rc)::value;
-          if (grp != Geo::rowner(r)) return;  // warp-uniform
-          constexpr int e0 = G::row_start[r], D = Geo::deg(r);
-          using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
-          WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
-          const int ci = r * Z + ln;
-          M m1o = 0, m2o = 0;
-          uint32_t wo = 0u;
-          if (!first) {
-            m1o = M1[ci];
-            m2o = m2[ci];
-            wo = (uint32_t)W[ln];
-          }
-          M mn1 = (M)INFINITY, mn2 = (M)INFINITY;
-          uint32_t arg = 0, sg = 0, syn = 0;
-          sfor<0, D>([&](auto pc) {
-            constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
-            // old message on this edge: +-(alpha*min1 | alpha*min2), sign
-            // bit of position p at bit D-1-p of the word
-            const M mag = qx_isarg<Geo, r, p>(wo) ? m2o : m1o;
-            const M cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
-            uint32_t o = i4 + 4u * s;  // byte offset of lane (i + s) mod Z
-            o = min(o, o - 4u * Z);
-            float tv;
-            if constexpr (c < KBC) {
-              tv = *reinterpret_cast<const float *>(reinterpret_cast<const char *>(T) + 4 * c * Z + o);
-            } else {
-              // degree-1 extension VN: its posterior is chan + its only message
-              const int v = c * Z + (int)(o >> 2);
-              const float ch = chn[v];
-              tv = first ? ch : qx_clip(qx_to_f32(qx_add((M)ch, cold)));
-              if (OUT && ES) ext[v - KBC * Z] = tv;
-            }
-            if (ES) syn ^= __float_as_uint(tv);
-            const M x = qx_sub((M)tv, cold);
-            if constexpr (Geo::EXACT) {
-              const double a = fabs(x);
-              const bool lt1 = a < mn1, lt2 = a < mn2;
-              const double t2 = lt2 ? a : mn2;
-              mn2 = lt1 ? mn1 : t2;
-              mn1 = lt1 ? a : mn1;
-              arg = lt1 ? Geo::argcode(r, p) : arg;
-            } else {  // one FMNMX per update in f32
-              const float a = fabsf(x);
-              arg = a < mn1 ? Geo::argcode(r, p) : arg;
-              mn2 = fminf(mn2, fmaxf(mn1, a));
-              mn1 = fminf(mn1, a);
-            }
-            sg = __funnelshift_l(qx_hi(x), sg, 1);  // signbit(x) in at bit 0
-          });
-          bad |= syn >> 31;
-          const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
-          M1[ci] = qx_mul(al, mn1);
-          m2[ci] = qx_mul(al, mn2);
-          W[ln] = (WT)(osg | arg);
-        });
-      }
-      if (ES && !first) {
-        // syndrome of the posteriors of iteration `it` (ldpc.py:155-160)
-        if (!__syncthreads_or(bad)) {
-          used = it;
-          break;
-        }
-      } else {
-        __syncthreads();
-      }
-      // ------------------------------------------------ variable-node phase
-      if (lane) {
-        const int j = ln;
-        uint32_t j8 = 8u * (uint32_t)j;
-        asm volatile("" : "+r"(j8));
-        sfor<0, KBC>([&](auto cc) {
-          constexpr int c = decltype(cc)::value;
-          if (grp != Geo::cowner(c)) return;  // warp-uniform
-          const float ch = chn[c * Z + j];
-          M x[Geo::cdeg(c)];
-          qx_vn_gather<Geo, c>(x, j8, qx_sm, m2);
-          T[c * Z + j] = qx_vn_total<Geo::cdeg(c)>(x, ch);
-        });
+  if (t < NC) flag[0][t] = flag[1][t] = 0u;
+  long long cw = -1;
+  int it = 0, used = 0;
+  bool need = lane;     // the slot wants a new codeword
+  bool refill = true;  // CTA-uniform: some slot finished in the last iteration
+  for (int g = 0;; ++g) {
+    if (refill) {
+      // ------------------------------------------------ refill finished slots
+      // (claimed one codeword ahead: the next one's LLR row is prefetched
+      // into L2 while this one decodes, so the refill's loads hit L2)
+      if (need && ts == 0) {
+        const long long c = g == 0 ? qx_claim(next, batch) : nxt[k];
+        cur[k] = c;
+        nxt[k] = c >= 0 ? qx_claim(next, batch) : -1;
+        errs[k] = 0u;
       }
       __syncthreads();
+      if (need) {
+        need = false;
+        cw = cur[k];
+        it = 0;
+        const long long nx = nxt[k];
+        if (nx >= 0) {
+          const char *nrow = reinterpret_cast<const char *>(llr + nx * (int64_t)row_len);
+          for (int b = 128 * ts; b < 4 * row_len; b += 128 * SLOT_T) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + b));
+        }
+        if (cw >= 0) {
+          const float *row = llr + cw * (int64_t)row_len;
+#pragma unroll 4
+          for (int v = ts; v < Geo::NB * Z; v += SLOT_T) {
+            const float ch = qx_chan(P, row, v, moth);
+            chn[v] = ch;
+            const int c = v / Z;
+            if (c < KBC) T[c * NZ + k * Z + (v - c * Z)] = ch;
+          }
+        }
+      }
+      if (!__syncthreads_or(lane && cw >= 0)) return;
     }
+    const bool act = lane && cw >= 0;
+    const bool first = it == 0;
+    uint32_t bad = 0;
+    // ------------------------------------------------ check-node phase
+    if (act) {
+      uint32_t i4 = 4u * (uint32_t)i;
+      // opaque per iteration: keeps the ~600 per-edge lane offsets from
+      // being hoisted out of the iteration loop (and spilled)
+      asm volatile("" : "+r"(i4));
+      const char *Tk = reinterpret_cast<const char *>(T) + k4;
+      sfor<0, MB>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        if (grp != Geo::rowner(r)) return;  // warp-uniform
+        constexpr int e0 = G::row_start[r], D = Geo::deg(r);
+        using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+        WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
+        M m1o = 0, m2o = 0;
+        uint32_t wo = 0u;
+        if (!first) {
+          m1o = M1l[r * NZ];
+          m2o = m2l[r * NZ];
+          wo = (uint32_t)W[ln];
+        }
+        M mn1 = (M)INFINITY, mn2 = (M)INFINITY;
+        uint32_t arg = 0, sg = 0, syn = 0;
+        sfor<0, D>([&](auto pc) {
+          constexpr int p = decltype(pc)::value, e = e0 + p, c = G::col[e], s = G::shift[e] % Z;
+          // old message on this edge: +-(alpha*min1 | alpha*min2), sign
+          // bit of position p at bit D-1-p of the word
+          const M mag = qx_isarg<Geo, r, p>(wo) ? m2o : m1o;
+          const M cold = qx_flip(mag, (wo << (32 - D + p)) & 0x80000000u);
+          uint32_t o = i4 + 4u * s;  // byte offset of lane (i + s) mod Z
+          o = min(o, o - 4u * Z);
+          float tv;
+          if constexpr (c < KBC) {
+            tv = *reinterpret_cast<const float *>(Tk + 4 * c * NZ + o);
+          } else {
+            // degree-1 extension VN: its posterior is chan + its only message
+            const int v = c * Z + (int)(o >> 2);
+            const float ch = chn[v];
+            tv = first ? ch : qx_clip(qx_to_f32(qx_add((M)ch, cold)));
+            if (OUT && ES) ext[(c - KBC) * NZ + k * Z + (int)(o >> 2)] = tv;
+          }
+          if (ES) syn ^= __float_as_uint(tv);
+          const M x = qx_sub((M)tv, cold);
+          if constexpr (Geo::EXACT) {
+            const double a = fabs(x);
+            const bool lt1 = a < mn1, lt2 = a < mn2;
+            const double t2 = lt2 ? a : mn2;
+            mn2 = lt1 ? mn1 : t2;
+            mn1 = lt1 ? a : mn1;
+            arg = lt1 ? Geo::argcode(r, p) : arg;
+          } else {  // one FMNMX per update in f32
+            const float a = fabsf(x);
+            arg = a < mn1 ? Geo::argcode(r, p) : arg;
+            mn2 = fminf(mn2, fmaxf(mn1, a));
+            mn1 = fminf(mn1, a);
+          }
+          sg = __funnelshift_l(qx_hi(x), sg, 1);  // signbit(x) in at bit 0
+        });
+        bad |= syn >> 31;
+        const uint32_t osg = (__popc(sg) & 1) ? sg ^ ((1u << D) - 1u) : sg;
+        M1l[r * NZ] = qx_mul(al, mn1);
+        m2l[r * NZ] = qx_mul(al, mn2);
+        W[ln] = (WT)(osg | arg);
+      });
+    }
+    // the slot's codeword passed the syndrome of the posteriors of its
+    // iteration `it` (ldpc.py:155-160): it stops before the variable update
+    bool conv = false;
+    if constexpr (ES && NC == 1) {
+      conv = !__syncthreads_or(bad) && act && !first;
+    } else {
+      if (ES && bad) flag[g & 1][k] = 1u;
+      __syncthreads();
+      if (ES) {
+        conv = act && !first && flag[g & 1][k] == 0u;
+        if (t < NC) flag[(g + 1) & 1][t] = 0u;
+      }
+    }
+    // ------------------------------------------------ variable-node phase
+    if (act && !conv) {
+      const int j = i;
+      uint32_t j8 = 8u * (uint32_t)j;
+      asm volatile("" : "+r"(j8));
+      sfor<0, KBC>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        if (grp != Geo::cowner(c)) return;  // warp-uniform
+        const float ch = chj[c * Z];
+        M x[Geo::cdeg(c)];
+        qx_vn_gather<Geo, c>(x, j8, k8, qx_sm, m2);
+        Tkj[c * NZ] = qx_vn_total<Geo::cdeg(c)>(x, ch);
+      });
+    }
+    bool fin = false;
+    if (act) {
+      if (conv) {
+        used = it;
+        fin = true;
+      } else if (++it == num_iter) {
+        used = num_iter;
+        fin = true;
+      }
+    }
+    refill = __syncthreads_or(fin);
+    if (!refill) continue;
 
-    // ------------------------------------------------ outputs
-    if (OUT && used == num_iter) {
+    // ------------------------------------------------ outputs of finished slots
+    if (OUT) {
       // extension posteriors after the last variable update: chan + c2v
-      if (lane) {
-        const int i = ln;
+      if (fin && used == num_iter) {
         sfor<4, MB>([&](auto rc) {
           constexpr int r = decltype(rc)::value;
           if (grp != Geo::rowner(r)) return;
@@ -384,53 +445,52 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           if constexpr (c >= KBC) {
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
             const WT *W = reinterpret_cast<const WT *>(qx_sm + Geo::woff(r));
-            const uint32_t w = W[i];
-            const M mag = qx_isarg<Geo, r, D - 1>(w) ? m2[r * Z + i] : M1[r * Z + i];
+            const uint32_t w = W[ln];
+            const M mag = qx_isarg<Geo, r, D - 1>(w) ? m2[r * NZ + ln] : M1[r * NZ + ln];
             const M cv = qx_flip(mag, (w << 31) & 0x80000000u);  // position D-1: bit 0
-            int j = i + s;
-            j = j >= Z ? j - Z : j;
-            const float ch = chn[c * Z + j];
-            ext[(c - KBC) * Z + j] = qx_clip(qx_to_f32(qx_add((M)ch, cv)));
+            int jj = i + s;
+            jj = jj >= Z ? jj - Z : jj;
+            const float ch = chn[c * Z + jj];
+            ext[(c - KBC) * NZ + k * Z + jj] = qx_clip(qx_to_f32(qx_add((M)ch, cv)));
           }
         });
       }
       __syncthreads();
     }
-    if (iters_used && t == 0) iters_used[cw] = used;
-    if (OUT && llr_out) {
-      float *o = llr_out + cw * (int64_t)P.n_full;
-      for (int v = t; v < P.n_full; v += NT) o[v] = -(v < KBC * Z ? T[v] : ext[v - KBC * Z]);
-    }
-    unsigned err = 0;
-    if (hard || ref) {
-      for (int v = t; v < hard_len; v += NT) {
-        const float tv = v < KBC * Z ? T[v] : (OUT ? ext[v - KBC * Z] : 0.0f);
-        const uint8_t h = (-tv) > 0.0f;
-        if (hard) hard[cw * (int64_t)hard_len + v] = h;
-        if (ref && v < P.k) err += (h != ref[cw * (int64_t)P.k + v]);
+    if (fin) {
+      if (iters_used && ts == 0) iters_used[cw] = used;
+      auto post = [&](int v) -> float {  // posterior of mother VN v of the slot's codeword
+        const int c = v / Z, jj = v - c * Z;
+        return c < KBC ? T[c * NZ + k * Z + jj] : (OUT ? ext[(c - KBC) * NZ + k * Z + jj] : 0.0f);
+      };
+      if (OUT && llr_out) {
+        float *o = llr_out + cw * (int64_t)P.n_full;
+        for (int v = ts; v < P.n_full; v += SLOT_T) o[v] = -post(v);
       }
-    }
-    if (ref && counts) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
-      if ((t & 31) == 0) red[t >> 5] = err;
-      __syncthreads();
-      if (t == 0) {
-        unsigned long long s = 0;
-        for (int w = 0; w < NT / 32; ++w) s += red[w];
-        if (s) {
-          atomicAdd(&counts[0], s);
-          atomicAdd(&counts[1], 1ULL);
+      unsigned err = 0;
+      if (hard || ref) {
+        for (int v = ts; v < hard_len; v += SLOT_T) {
+          const uint8_t h = (-post(v)) > 0.0f;
+          if (hard) hard[cw * (int64_t)hard_len + v] = h;
+          if (ref && v < P.k) err += (h != ref[cw * (int64_t)P.k + v]);
         }
       }
+      if (ref && counts && err) atomicAdd(&errs[k], err);
+      need = true;
     }
-    __syncthreads();
+    if (ref && counts) {
+      __syncthreads();
+      if (fin && ts == 0 && errs[k]) {
+        atomicAdd(&counts[0], (unsigned long long)errs[k]);
+        atomicAdd(&counts[1], 1ULL);
+      }
+    }
   }
 }
 
-// one decoder instance: persistent grid; the exact (f64) decoder keeps an L2
-// slice of min2 per CTA, the fp32 one keeps everything but the channel in
-// shared memory
+// one decoder instance: persistent grid of NC-slot CTAs; the exact (f64)
+// decoder keeps an L2 slice of min2 per CTA, the fp32 one keeps everything
+// but the channel in shared memory
 template <class G, int Z, int NTL, class M = double>
 int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_iter, double alpha, int early_stop,
                     int mother, uint8_t *hard, int hard_len, float *llr_out, int32_t *iters_used, const uint8_t *ref,
@@ -442,15 +502,17 @@ int launch_qc_exact(const QcChanParams &P, const float *llr, int64_t B, int num_
                          : (out ? k_qc_exact<Geo, false, true> : k_qc_exact<Geo, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(exact smem attr)");
+  if (num_iter < 1) return fail(LS_EINVAL, "num_iter must be >= 1");  // the slot loop needs one iteration
+  if (B <= 0) return LS_OK;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Geo::NT, Geo::SMEM);
-  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), B);
-  if (grid <= 0) return LS_OK;
-  const size_t m2_bytes = Geo::EXACT ? sizeof(M) * (size_t)grid * Geo::MB * Z : 0;
-  const size_t ext_bytes = out ? sizeof(float) * (size_t)grid * Geo::NEXT * Z : 0;
-  const size_t ch_bytes = sizeof(float) * (size_t)grid * Geo::NB * Z;
+  // enough CTAs for every slot to start with a codeword when the batch is small
+  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), (B + Geo::NC - 1) / Geo::NC);
+  const size_t m2_bytes = Geo::EXACT ? sizeof(M) * (size_t)grid * Geo::MB * Geo::NZ : 0;
+  const size_t ext_bytes = out ? sizeof(float) * (size_t)grid * Geo::NEXT * Geo::NZ : 0;
+  const size_t ch_bytes = sizeof(float) * (size_t)grid * Geo::NB * Geo::NZ;
   char *ws = nullptr;
   retain_pool_memory();
   e = cudaMallocAsync((void **)&ws, 256 + m2_bytes + ext_bytes + ch_bytes, s);

@@ -141,6 +141,34 @@ def test_qc_exact_persistent_batch_equals_csr_engine():
         assert np.array_equal(a[2], b[2])
 
 
+@pytest.mark.parametrize("k,n,m,ebno,B", [(256, 512, 2, 4.0, 4501), (256, 512, 2, 4.0, 3),
+                                          (4096, 8192, 2, 3.0, 701)])
+def test_qc_exact_codeword_slots_equal_csr_engine(k, n, m, ebno, B):
+    """Several codewords per CTA in lockstep (Z < 384: 14 slots at Z = 26, 2
+    at Z = 192), each slot refilled when its codeword stops: batches larger
+    than all slots together and smaller than one CTA's, odd sizes, codewords
+    stopping at different iterations.  Everything equal to the CSR engine and
+    the fused counts equal to the oracle's."""
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    bits, llr = _llrs(k, n, m, ebno, B, 21)
+    mother = oc.derate_match(llr)
+    for variant in VARIANTS:
+        for es in (True, False):
+            a = lb.bp_decode(mother, code.pcm, 20, variant, 0.75, es, return_iters=True, engine="qc")
+            b = lb.bp_decode(mother, code.pcm, 20, variant, 0.75, es, return_iters=True, engine="csr")
+            assert np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+            assert np.array_equal(a[1], b[1])
+            assert np.array_equal(a[2], b[2])
+            if es and B > 100:
+                assert len(np.unique(a[2])) > 3  # stops spread over iterations
+        r = LD.qc_decode(llr, code, 20, variant, 0.75, early_stop=True, precision="exact", ref_bits=bits,
+                         want_iters=True)
+        assert np.array_equal(r["hard"].cpu().numpy(), b[1][:, :k])
+        be, ble = O.count_errors(bits, b[1][:, :k])
+        assert [int(x) for x in r["counts"].cpu()] == [be, ble]
+
+
 def test_qc_exact_rejects_sum_product_and_unknown_engine():
     code = lb.LdpcCode5G(256, 512)
     llr = np.zeros((2, code.n_full), np.float32)

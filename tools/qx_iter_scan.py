@@ -19,15 +19,22 @@ p.add_argument("--n", type=int, default=16896)
 p.add_argument("--m", type=int, default=4)
 p.add_argument("--ebno", type=float, default=6.0)
 p.add_argument("--precision", default="exact")
+p.add_argument("--lib", default=None, help="load this liblinksim_b200.so instead (A/B of two builds)")
+p.add_argument("--iters", default="1,2,5,10,20")
+p.add_argument("--reps", type=int, default=1)
+p.add_argument("--modes", default="fixed,es")
 a = p.parse_args()
+if a.lib:
+    from paper_2203_11854_b200 import _lib
+    _lib.LIB_PATH = os.path.abspath(a.lib)
 cfg = lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": a.k, "n": a.n, "decoder": {"mode": "fast"}},
                               "modulation": {"kind": "qam", "bits_per_symbol": a.m},
                               "sweep": {"ebno_db": [a.ebno], "batch_size": a.batch}})
 pipe = lb.Pipeline(cfg)
 payload, llr = pipe._llr(a.ebno, a.batch, lb.RngStream(1, 2))
 res = {}
-for es in (False, True):
-    for it in (1, 2, 5, 10, 20):
+for es in [m == "es" for m in a.modes.split(",")]:
+    for it in [int(x) for x in a.iters.split(",")]:
         def run():
             return LD.qc_decode(llr, pipe.ldpc, it, "min-sum", 0.75, early_stop=es, precision=a.precision,
                                 ref_bits=payload, want_hard=False, want_iters=es)
@@ -35,11 +42,12 @@ for es in (False, True):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        r = run()
+        for _ in range(a.reps):
+            r = run()
         e1.record()
         torch.cuda.synchronize()
         key = f"{'es' if es else 'fixed'}_{it}"
-        res[key] = {"ms": e0.elapsed_time(e1)}
+        res[key] = {"ms": e0.elapsed_time(e1) / a.reps}
         if es:
             res[key]["mean_iters"] = float(r["iters"].float().mean())
         print(key, res[key], flush=True)
