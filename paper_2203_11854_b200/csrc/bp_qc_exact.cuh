@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         errs[k] = 0u;
       }
       __syncthreads();
+      if (NC == 1) it = 0;  // one slot: keep the iteration state CTA-uniform
       if (need) {
         need = false;
         cw = cur[k];
@@ -315,6 +316,15 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           for (int b = 128 * ts; b < 4 * row_len; b += 128 * SLOT_T) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + b));
         }
         if (cw >= 0) {
+          // zero check state: the first iteration's old messages are +0
+          if constexpr (!ES) sfor<0, MB>([&](auto rc) {
+            constexpr int r = decltype(rc)::value;
+            if (grp != Geo::rowner(r)) return;
+            using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
+            M1l[r * NZ] = (M)0;
+            m2l[r * NZ] = (M)0;
+            reinterpret_cast<WT *>(qx_sm + Geo::woff(r))[ln] = (WT)0;
+          });
           const float *row = llr + cw * (int64_t)row_len;
 #pragma unroll 4
           for (int v = ts; v < Geo::NB * Z; v += SLOT_T) {
@@ -327,7 +337,8 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       }
       if (!__syncthreads_or(lane && cw >= 0)) return;
     }
-    const bool act = lane && cw >= 0;
+    // (one slot: the CTA returned above unless its codeword is live)
+    const bool act = NC == 1 ? lane : lane && cw >= 0;
     const bool first = it == 0;
     uint32_t bad = 0;
     // ------------------------------------------------ check-node phase
@@ -343,9 +354,12 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         constexpr int e0 = G::row_start[r], D = Geo::deg(r);
         using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
         WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
+        // old messages are +0 in the first iteration: fixed-iteration kernels
+        // zero a refilled slot's state (no branch in the hot loop), early-stop
+        // ones skip the loads (a different register allocation wins there)
         M m1o = 0, m2o = 0;
         uint32_t wo = 0u;
-        if (!first) {
+        if (!ES || !first) {
           m1o = M1l[r * NZ];
           m2o = m2l[r * NZ];
           wo = (uint32_t)W[ln];
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
     // iteration `it` (ldpc.py:155-160): it stops before the variable update
     bool conv = false;
     if constexpr (ES && NC == 1) {
-      conv = !__syncthreads_or(bad) && act && !first;
+      conv = !__syncthreads_or(bad) && !first;
     } else {
       if (ES && bad) flag[g & 1][k] = 1u;
       __syncthreads();
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       });
     }
     bool fin = false;
-    if (act) {
+    if (NC == 1 || act) {
       if (conv) {
         used = it;
         fin = true;
