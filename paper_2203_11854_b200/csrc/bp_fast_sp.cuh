@@ -363,27 +363,98 @@ __device__ __forceinline__ float sp32_pairwise(const float *x) {  // numpy pairw
   }
 }
 
-template <class Geo, bool ES>
-__global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
-    k_qc_sp32(const QcChanParams P, const Geo geo, const float *__restrict__ llr, int num_iter,
+// Graph tables of the f32 kernel, built at compile time and passed by value
+// (kernel parameter space): rows grouped by degree and core/extension
+// columns grouped by live degree, so that one copy of a row (column) body
+// per degree serves every row (column) of that degree and both thread
+// groups.  Fully unrolled per-row code (260 KB) left the kernel waiting on
+// instruction fetch with its 12 warps per SM (`no_instruction` 4.0 of 7.8
+// cycles per issue, profiles/r02/ncu_sp32_v1_summary.txt).
+template <class G, int Z, int R>
+struct Sp32Tab {
+  static constexpr int NE = G::row_start[R], NCOL = G::KB + (R > 4 ? R : 4);
+  static constexpr int rdeg(int r) { return G::row_start[r + 1] - G::row_start[r]; }
+  static constexpr int cdeg(int c) {  // entries of column c in rows < R
+    int n = 0;
+    for (int q = G::col_start[c]; q < G::col_start[c + 1]; ++q) n += G::row[G::col_entry[q]] < R;
+    return n;
+  }
+  static constexpr int maxr() {
+    int m = 0;
+    for (int r = 0; r < R; ++r) m = rdeg(r) > m ? rdeg(r) : m;
+    return m;
+  }
+  static constexpr int maxc() {
+    int m = 0;
+    for (int c = 0; c < NCOL; ++c) m = cdeg(c) > m ? cdeg(c) : m;
+    return m;
+  }
+  static constexpr int MAXR = maxr(), MAXC = maxc();
+  static constexpr bool has_rdeg(int d) {
+    for (int r = 0; r < R; ++r)
+      if (rdeg(r) == d) return true;
+    return false;
+  }
+  static constexpr bool has_cdeg(int d) {
+    for (int c = 0; c < NCOL; ++c)
+      if (cdeg(c) == d) return true;
+    return false;
+  }
+  uint16_t re0[R];             // first entry of each row, rows in degree order
+  uint16_t roff[MAXR + 2];     // rows of degree d: re0[roff[d] .. roff[d+1])
+  uint16_t ccol[NCOL];         // columns in live-degree order
+  uint16_t coff[MAXC + 2];     // columns of degree d: ccol[coff[d] .. coff[d+1])
+  uint16_t cst[NCOL];          // first live entry of each of them in cent
+  uint2 cent[NE];              // their live entries (e * Z, Z - shift mod Z), column by column,
+                               // ascending check order
+  uint2 rcs[NE];               // entry e: (byte offset of its column in the posteriors, 4 * (shift mod Z))
+  constexpr Sp32Tab() : re0{}, roff{}, ccol{}, coff{}, cst{}, cent{}, rcs{} {
+    int k = 0;
+    for (int d = 0; d <= MAXR + 1; ++d) {
+      roff[d] = (uint16_t)k;
+      for (int r = 0; r < R && d <= MAXR; ++r)
+        if (rdeg(r) == d) re0[k++] = (uint16_t)G::row_start[r];
+    }
+    k = 0;
+    int q = 0;
+    for (int d = 0; d <= MAXC + 1; ++d) {
+      coff[d] = (uint16_t)k;
+      for (int c = 0; c < NCOL && d <= MAXC; ++c) {
+        if (cdeg(c) != d) continue;
+        cst[k] = (uint16_t)q;
+        ccol[k++] = (uint16_t)c;
+        for (int t = G::col_start[c]; t < G::col_start[c + 1]; ++t) {
+          const int e = G::col_entry[t];
+          if (G::row[e] < R) cent[q++] = uint2{(uint32_t)(e * Z), (uint32_t)(Z - G::shift[e] % Z)};
+        }
+      }
+    }
+    for (int e = 0; e < NE; ++e)
+      rcs[e] = uint2{4u * (uint32_t)Z * (uint32_t)G::col[e], 4u * (uint32_t)(G::shift[e] % Z)};
+  }
+};
+
+template <class G, int Z, int R, int SPLIT, bool ES>
+__global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z, R, SPLIT>::MINB)
+    k_qc_sp32(const QcChanParams P, const Sp32Tab<G, Z, R> tab, const float *__restrict__ llr, int num_iter,
               uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
               const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts) {
-  using G = typename Geo::G;
-  constexpr int SPLIT = Geo::SPLIT;
-  const int Z = geo.z(), NT = geo.nt(), NCOLZ = geo.ncol() * Z;
+  using S = QcShapeSP<G, Z, R, SPLIT>;
+  using Tab = Sp32Tab<G, Z, R>;
+  constexpr int NT = S::NT, NT1 = S::NT1, NCOLZ = S::NCOL * Z;
   extern __shared__ float smf[];
-  float *c2v = smf;                         // [NE][Z]
-  float *tot = smf + (size_t)geo.ne() * Z;  // [NCOL][Z]
-  char *const totb = reinterpret_cast<char *>(tot);
+  float *c2v = smf;                     // [NE][Z]
+  float *tot = smf + (size_t)S::NE * Z;  // [NCOL][Z]
+  const char *const totb = reinterpret_cast<const char *>(tot);
   const int t = threadIdx.x;
-  const int h = t / geo.nt1();
-  const int i = t - h * geo.nt1();
-  const bool lane = geo.full_lanes() || i < Z;
+  const int h = t / NT1;  // thread group: every SPLIT-th row / column of each degree class
+  const int i = t - h * NT1;
+  const bool lane = NT1 == Z || i < Z;
   const int64_t b = blockIdx.x;
   const float *row = llr + b * (int64_t)P.n;
 
   for (int v = t; v < NCOLZ; v += NT) tot[v] = chan_value(P, row, v) * kLog2e;
-  for (int q = t; q < geo.ne() * Z; q += NT) c2v[q] = 0.0f;
+  for (int q = t; q < S::NE * Z; q += NT) c2v[q] = 0.0f;
   __syncthreads();
 
   // one check-node phase; FIRST = the reference's float32 first pass
@@ -391,28 +462,25 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     constexpr bool first = decltype(first_c)::value;
     uint32_t synx = 0;
     if (lane) {
-      sfor<0, SPLIT>([&](auto hc) {
-        constexpr int H = decltype(hc)::value;
-        if (h != H) return;
-        const unsigned i2 = 2u * (tid_volatile() - H * geo.nt1());
-        const int il = (int)(i2 >> 1);
-        sfor<0, (Geo::RB + SPLIT - 1) / SPLIT>([&](auto jc) {
-          constexpr int r = decltype(jc)::value * SPLIT + H;
-          if constexpr (r < Geo::RB) {
-            if (!geo.template live<r>()) return;
-            constexpr int e0 = G::row_start[r], e1 = G::row_start[r + 1], d = e1 - e0;
-            // first pass: phi per edge; later: u = 2^-y, n = 1 - u per edge and
-            // the prefix products (pn, pp) = (N, P) of the edges before it
+      uint32_t i4 = 4u * (uint32_t)i;
+      asm volatile("" : "+r"(i4));
+      sfor<1, Tab::MAXR + 1>([&](auto dc) {
+        constexpr int d = decltype(dc)::value;
+        if constexpr (Tab::has_rdeg(d)) {
+          for (int rr = tab.roff[d] + h; rr < tab.roff[d + 1]; rr += SPLIT) {
+            const int e0 = tab.re0[rr];
             float ph[first ? d : 1], uu[first ? 1 : d], nn[first ? 1 : d], pn[first ? 1 : d], pp[first ? 1 : d];
             float na = 1.0f, pa = 0.0f;
             uint32_t sg = 0, hs = 0;
-            sfor<e0, e1>([&](auto ec) {
-              constexpr int e = decltype(ec)::value;
-              constexpr int p = e - e0;
-              // the 2-byte-element offsets of the fp16 geometry, doubled
-              const float tv = *reinterpret_cast<const float *>(totb + 2u * geo.template off<e>(i2));
+#pragma unroll
+            for (int p = 0; p < d; ++p) {
+              const int e = e0 + p;
+              const uint2 cs = tab.rcs[e];
+              uint32_t o = i4 + cs.y;
+              o = min(o, o - 4u * Z);
+              const float tv = *reinterpret_cast<const float *>(totb + cs.x + o);
               if constexpr (ES) hs ^= __float_as_uint(tv);
-              const float x = tv - c2v[geo.template ez<e>() + il];
+              const float x = tv - c2v[e * Z + i];
               sg |= (__float_as_uint(x) >> 31) << p;
               if constexpr (first) {
                 ph[p] = sp32_phi_first(fabsf(x));
@@ -427,33 +495,32 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
                 pa = fmaf(2.0f * u, na, fmaf(pa, u, pa));
                 na *= nn[p];
               }
-            });
+            }
             const uint32_t par = __popc(sg) & 1u;
             if constexpr (first) {  // the reference's f32 pass: psum in pairwise order, then psum - pmag
               const float ps = __fadd_rn(ph[0], sp32_pairwise<d - 1>(ph + 1));
-              sfor<e0, e1>([&](auto ec) {
-                constexpr int e = decltype(ec)::value;
-                constexpr int p = e - e0;
+#pragma unroll
+              for (int p = 0; p < d; ++p) {
                 const float m = fminf(sp32_phi_first(__fsub_rn(ps, ph[p])), kMsgClip2);
                 const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
-                c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
-              });
+                c2v[(e0 + p) * Z + i] = __uint_as_float(__float_as_uint(m) ^ neg);
+              }
             } else {
               // exclusive (N, P) of every edge from the prefix (pn, pp) and a
               // running suffix (nb, pb): N_ex = N_a N_b, P_ex = P_a Q_b + N_a P_b
               float nb = 1.0f, pb = 0.0f;
-              sfor<0, d>([&](auto qc) {
-                constexpr int p = d - 1 - decltype(qc)::value, e = e0 + p;
+#pragma unroll
+              for (int p = d - 1; p >= 0; --p) {
                 const float m = sp32_msg(pn[p] * nb, fmaf(pp[p], nb + pb, pn[p] * pb));
                 const uint32_t neg = ((par ^ (sg >> p)) & 1u) << 31;
-                c2v[geo.template ez<e>() + il] = __uint_as_float(__float_as_uint(m) ^ neg);
+                c2v[(e0 + p) * Z + i] = __uint_as_float(__float_as_uint(m) ^ neg);
                 pb = fmaf(2.0f * uu[p], nb, fmaf(pb, uu[p], pb));
                 nb *= nn[p];
-              });
+              }
             }
             if constexpr (ES) synx |= hs;
           }
-        });
+        }
       });
     }
     return synx;
@@ -470,26 +537,25 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     } else {
       __syncthreads();
     }
+    // ------------------------------------------------ variable-node phase (gather)
     if (lane) {
-      sfor<0, SPLIT>([&](auto hc) {
-        constexpr int H = decltype(hc)::value;
-        if (h != H) return;
-        const int j = (int)tid_volatile() - H * geo.nt1();
-        sfor<0, (Geo::NCOL_MAX + SPLIT - 1) / SPLIT>([&](auto cc) {
-          constexpr int c = decltype(cc)::value * SPLIT + H;
-          if constexpr (c < Geo::NCOL_MAX) {
-            if (c >= geo.ncol()) return;
+      const int j = i;
+      sfor<1, Tab::MAXC + 1>([&](auto dc) {
+        constexpr int d = decltype(dc)::value;
+        if constexpr (Tab::has_cdeg(d)) {
+          for (int cc = tab.coff[d] + h; cc < tab.coff[d + 1]; cc += SPLIT) {
+            const int c = tab.ccol[cc];
+            const int q0 = tab.cst[cc];
             float sum = chan_value(P, row, c * Z + j) * kLog2e;
-            constexpr int q0 = G::col_start[c], q1 = G::col_start[c + 1];
-            sfor<q0, q1>([&](auto qc) {
-              constexpr int e = G::col_entry[decltype(qc)::value];
-              if constexpr (G::row[e] < Geo::RB) {
-                if (geo.template live<G::row[e]>()) sum += c2v[geo.template src<e>(j)];
-              }
-            });
+#pragma unroll
+            for (int q = 0; q < d; ++q) {
+              const uint2 ez = tab.cent[q0 + q];
+              const unsigned a = (unsigned)j + ez.y;
+              sum += c2v[ez.x + min(a, a - (unsigned)Z)];
+            }
             tot[c * Z + j] = fminf(fmaxf(sum, -kClip2), kClip2);
           }
-        });
+        }
       });
     }
     __syncthreads();
@@ -507,7 +573,7 @@ __global__ void __launch_bounds__(Geo::NT_MAX, Geo::MINB)
     if (ref) err += (hd != ref[b * (int64_t)P.k + v]);
   }
   if (ref && counts) {
-    __shared__ unsigned red[Geo::NT_MAX / 32];
+    __shared__ unsigned red[NT / 32];
 #pragma unroll
     for (int o = 16; o; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
     if ((t & 31) == 0) red[t >> 5] = err;
@@ -529,19 +595,20 @@ int launch_qc_sp32(const QcChanParams &P, const float *llr, int64_t B, int num_i
                    unsigned long long *counts, cudaStream_t s) {
   (void)alpha;
   using S = QcShapeSP<G, Z, R, SPLIT>;
+  using Tab = Sp32Tab<G, Z, R>;
+  static_assert(sizeof(Tab) + sizeof(QcChanParams) + 96 <= 32000, "kernel parameters too large");
   constexpr size_t smem = 2 * S::SMEM;  // f32 messages and posteriors
   static_assert(smem <= 227 * 1024, "f32 sum-product messages do not fit in shared memory");
-  using Geo = SpGeoCT<G, Z, R, SPLIT>;
-  auto kern = early_stop ? k_qc_sp32<Geo, true> : k_qc_sp32<Geo, false>;
+  static constexpr Tab tab{};
+  auto kern = early_stop ? k_qc_sp32<G, Z, R, SPLIT, true> : k_qc_sp32<G, Z, R, SPLIT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
   for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
     const int64_t nb = B - b0 < 0x7fffffff ? B - b0 : 0x7fffffff;
-    kern<<<(unsigned)nb, S::NT, smem, s>>>(P, Geo{}, llr + b0 * P.n, num_iter,
-                                            hard_k ? hard_k + b0 * P.k : nullptr,
+    kern<<<(unsigned)nb, S::NT, smem, s>>>(P, tab, llr + b0 * P.n, num_iter, hard_k ? hard_k + b0 * P.k : nullptr,
                                             llr_out ? llr_out + b0 * P.n_full : nullptr,
-                                            iters_used ? iters_used + b0 : nullptr,
-                                            ref ? ref + b0 * P.k : nullptr, counts);
+                                            iters_used ? iters_used + b0 : nullptr, ref ? ref + b0 * P.k : nullptr,
+                                            counts);
   }
   e = cudaGetLastError();
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
