@@ -15,19 +15,20 @@
 // (row parity already XORed in); (-alpha)*x == -(alpha*x) exactly, so the
 // sign is a bit flip.
 //
-// Data layout for one codeword per CTA (persistent, one CTA per SM at
-// Z = 384):
-//   shared  M1 [MB][Z] f64     alpha*min1 of every check
-//           W  [MB][Z] u16/u32 outgoing signs (position p at bit deg-1-p)
+// Data layout (persistent CTAs; NC codewords per CTA in lockstep, lane
+// k * Z + i of every state array = lane i of slot k; NC = 1 at Z = 384):
+//   shared  M1 [MB][NC*Z] f64  alpha*min1 of every check
+//           W  [MB][NC*Z] u16/u32 outgoing signs (position p at bit deg-1-p)
 //                              | argmin, one-hot at bit deg + p for rows of
 //                              degree <= 16, else the position << deg
-//           T  [KBC][Z] f32    posteriors of the core columns (systematic +
+//           T  [KBC][NC*Z] f32 posteriors of the core columns (systematic +
 //                              4 core parity; KBC = k_b + 4)
-//   global  m2 [MB][Z] f64     alpha*min2 per check, one slice per CTA: read
+//   global  m2 [MB][NC*Z] f64  alpha*min2 per check, one slice per CTA: read
 //                              once per check in the CN phase and once per
 //                              argmin edge in the VN phase, L2-resident
-//           channel LLRs       read from the input row each iteration (L2)
-// Config 2 (BG1, Z = 384): 141,312 + 38,400 + 39,936 = 219,648 B of shared
+//           chn [NC][NB][Z]    channel values -derate(llr) of each slot's
+//                              codeword, formed once per codeword (L2)
+// Config 2 (BG1, Z = 384): 141,312 + 45,312 + 39,936 = 226,560 B of shared
 // memory.  The degree-1 extension columns keep no posterior: their value
 // clip(f32(chan + c2v)) is formed inside the check update of their row.
 //
