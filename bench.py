@@ -29,14 +29,14 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 K_INFO, N_TX, M_BITS = 8448, 16896, 4
-# kernels of one headline step (ncu launch list, profiles/r02/launches_bench_r2.csv):
+# kernels of one headline step (ncu launch list, profiles/r02/launches_bench_r2h.csv):
 # binary_source, encoder, mapper, 5 numpy-ziggurat kernels, noise apply, demapper, exact decoder
 GPU_LAUNCHES_PER_STEP = 11
 # DRAM bytes (read + write) per codeword of k_qc_exact<BG1,384,2>, from the
 # ncu --set full capture of the bench's own 65,536-codeword decoder launch
-# (profiles/r02/ncu_k_qc_exact_bench_*: 5.103 GB read + 0.125 GB written);
-# the messages never leave the SM, DRAM sees the LLR input and the counts
-EXACT_TRAFFIC_PER_CW = (5_103_239_000 + 125_331_712) / 65536
+# (profiles/r02/ncu_k_qc_exact_bench_r2h_summary.txt: 5.028 GB read + 18.2 MB
+# written); the messages never leave the SM, DRAM sees the LLR input and the counts
+EXACT_TRAFFIC_PER_CW = (5_027_535_000 + 18_208_768) / 65536
 METRIC = "decoded info Gbit/s (LDPC BG1, 20 iters) at 1/2/4/8 B200 vs CPU ref; %roofline"
 
 
@@ -290,10 +290,10 @@ def run_b200(a, rank, world, local_rank):
                                        "min2 and channel in an L2 slice per SM); the kernel is bound by the "
                                        "ALU issue pipe, not HBM (ncu in profiles/r02)"),
             "issue_roofline": {"note": "from the ncu --set full capture of this decoder launch at B=65,536 "
-                                       "(profiles/r02/ncu_k_qc_exact_bench_summary.txt)",
-                               "warp_instructions_per_launch": 185_036_924_212, "ipc": 2.69, "ipc_peak": 4.0,
-                               "issue_frac": 2.69 / 4.0, "alu_pipe_frac": 0.711,
-                               "dram_bytes_per_launch": 5_228_570_712},
+                                       "(profiles/r02/ncu_k_qc_exact_bench_r2h_summary.txt)",
+                               "warp_instructions_per_launch": 180_086_345_950, "ipc": 2.67, "ipc_peak": 4.0,
+                               "issue_frac": 2.67 / 4.0, "alu_pipe_frac": 0.691,
+                               "dram_bytes_per_launch": 5_045_743_768},
             "clocks": clk.summary(),
             "errors_in_timed_region": {"bit_errors": errs[0], "block_errors": errs[1],
                                        "blocks": world * B * a.steps}}
