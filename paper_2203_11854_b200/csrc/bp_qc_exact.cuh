@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
   float *T = reinterpret_cast<float *>(qx_sm + Geo::T_OFF);
   __shared__ long long cur[NC], nxt[NC];
   __shared__ unsigned errs[NC];
+  __shared__ bool rf[NC];  // slot refilled in this refill step
   __shared__ uint32_t flag[2][NC];  // per-slot syndrome flags, double-buffered by CTA iteration
   const int t = threadIdx.x, grp = t / NT1, ln = t - grp * NT1;
   const bool lane = ln < NZ;
@@ -299,11 +300,14 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       // ------------------------------------------------ refill finished slots
       // (claimed one codeword ahead: the next one's LLR row is prefetched
       // into L2 while this one decodes, so the refill's loads hit L2)
-      if (need && ts == 0) {
-        const long long c = g == 0 ? qx_claim(next, batch) : nxt[k];
-        cur[k] = c;
-        nxt[k] = c >= 0 ? qx_claim(next, batch) : -1;
-        errs[k] = 0u;
+      if (lane && ts == 0) {
+        if (need) {
+          const long long c = g == 0 ? qx_claim(next, batch) : nxt[k];
+          cur[k] = c;
+          nxt[k] = c >= 0 ? qx_claim(next, batch) : -1;
+          errs[k] = 0u;
+        }
+        rf[k] = need;
       }
       __syncthreads();
       if (NC == 1) it = 0;  // one slot: keep the iteration state CTA-uniform
@@ -326,13 +330,33 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
             m2l[r * NZ] = (M)0;
             reinterpret_cast<WT *>(qx_sm + Geo::woff(r))[ln] = (WT)0;
           });
-          const float *row = llr + cw * (int64_t)row_len;
+          if constexpr (NC == 1) {
+            const float *row = llr + cw * (int64_t)row_len;
 #pragma unroll 4
-          for (int v = ts; v < Geo::NB * Z; v += SLOT_T) {
+            for (int v = ts; v < Geo::NB * Z; v += SLOT_T) {
+              const float ch = qx_chan(P, row, v, moth);
+              chn[v] = ch;
+              const int c = v / Z;
+              if (c < KBC) T[c * NZ + (v - c * Z)] = ch;
+            }
+          }
+        }
+      }
+      if constexpr (NC > 1) {
+        // the channel values of every refilled slot, by all threads of the
+        // CTA (the other slots wait at the next barrier anyway): the load is
+        // latency-bound, so more threads per codeword shorten it
+        for (int kk = 0; kk < NC; ++kk) {
+          const long long ck = rf[kk] ? cur[kk] : -1;  // CTA-uniform
+          if (ck < 0) continue;
+          const float *row = llr + ck * (int64_t)row_len;
+          float *chk = chws + ((size_t)blockIdx.x * NC + kk) * Geo::NB * Z;
+#pragma unroll 4
+          for (int v = t; v < Geo::NB * Z; v += Geo::NT) {
             const float ch = qx_chan(P, row, v, moth);
-            chn[v] = ch;
+            chk[v] = ch;
             const int c = v / Z;
-            if (c < KBC) T[c * NZ + k * Z + (v - c * Z)] = ch;
+            if (c < KBC) T[c * NZ + kk * Z + (v - c * Z)] = ch;
           }
         }
       }
