@@ -175,7 +175,8 @@ int ls_bp_decode(const ls_graph *g, const void *llr, int is_f64, int64_t batch, 
  * (core.py:93-99), messages on chip.  The fp16x2 kernels run a pair of
  * codewords per CTA (persistent CTAs, one or two slots per SM); the exact /
  * fp32 full-graph kernel (LS_QC_EXACT / LS_QC_FULL32) one codeword per
- * persistent CTA.  llr [B,n] f32
+ * persistent CTA at Z = 384 and 384 / Z codewords in lockstep below it.
+ * llr [B,n] f32
  * rate-matched.  Outputs (all nullable): hard_k [B,k] info bits,
  * llr_out [B,n_full] f32 mother LLRs (ln p1/p0), iters_used [B],
  * counts[2] += (bit errors, block errors) against ref_bits [B,k].
