@@ -42,12 +42,54 @@ def oracle_decode(llr, oc, variant, threads, chunk):
             np.concatenate([p[2] for p in parts]))
 
 
+# whole exact-mode Pipeline.run_batch (payload, encoder, mapper, numpy-exact
+# noise, f64 demapper, exact decoder) against the oracle's run_batch:
+# (k, n, bits per symbol, Eb/N0, variant, batches, batch size)
+CHAIN_CASES = [
+    (256, 512, 2, 3.5, "min-sum", 64, 256),
+    (8448, 16896, 4, 5.6, "min-sum", 32, 64),
+    (4096, 8192, 2, 3.0, "scaled-min-sum", 32, 128),
+    (4096, 12288, 6, 7.5, "min-sum", 32, 64),
+]
+
+
+def chain_campaign(a):
+    res = []
+    for k, n, m, ebno, variant, nb, bs in CHAIN_CASES:
+        nb = max(2, int(nb * a.scale))
+        cfg = lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": k, "n": n,
+                                               "decoder": {"variant": variant, "num_iter": 20}},
+                                      "modulation": {"kind": "qam", "bits_per_symbol": m},
+                                      "sweep": {"ebno_db": [ebno], "batch_size": bs}})
+        pipe = lb.Pipeline(cfg)
+        seed = 1000 + k
+        gpu = [pipe.run_batch(ebno, bs, lb.RngStream(seed, (1 << 32) | (b + 1))) for b in range(nb)]
+        t0 = time.perf_counter()
+        with concurrent.futures.ThreadPoolExecutor(a.threads) as ex:
+            ref = list(ex.map(lambda b: O.run_batch(k, n, m, ebno, bs, seed, (1 << 32) | (b + 1), variant),
+                              range(nb)))
+        el = time.perf_counter() - t0
+        same_p = sum(int(np.array_equal(g[0], r[0])) for g, r in zip(gpu, ref))
+        same_d = sum(int(np.array_equal(g[1], r[1])) for g, r in zip(gpu, ref))
+        rec = {"k": k, "n": n, "m": m, "ebno_db": ebno, "variant": variant, "batches": nb, "batch_size": bs,
+               "codewords": nb * bs, "identical_payload_batches": same_p, "identical_decoded_batches": same_d,
+               "block_errors": int(sum((r[0] != r[1]).any(axis=1).sum() for r in ref)),
+               "oracle_seconds": round(el, 1)}
+        rec["all_identical"] = same_p == nb and same_d == nb
+        res.append(rec)
+        print(json.dumps(rec), file=sys.stderr, flush=True)
+    return res
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--scale", type=float, default=1.0, help="multiply every case's codeword count")
     p.add_argument("--threads", type=int, default=os.cpu_count() or 8)
+    p.add_argument("--chain", action="store_true", help="also compare whole exact-mode run_batch chains")
     a = p.parse_args()
     out = {"threads": a.threads, "cases": []}
+    if a.chain:
+        out["chain_cases"] = chain_campaign(a)
     for k, n, m, ebno, B in CASES:
         B = max(8, int(B * a.scale))
         cfg = lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": k, "n": n},
@@ -76,7 +118,7 @@ def main():
                                     and rec["identical_iters"] == B)
             out["cases"].append(rec)
             print(json.dumps(rec), file=sys.stderr, flush=True)
-    out["all_identical"] = all(c["all_identical"] for c in out["cases"])
+    out["all_identical"] = all(c["all_identical"] for c in out["cases"] + out.get("chain_cases", []))
     out["codewords_compared"] = sum(c["codewords"] for c in out["cases"])
     print(json.dumps(out, indent=1))
 
