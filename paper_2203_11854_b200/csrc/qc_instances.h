@@ -75,7 +75,11 @@
 // mother graph; codes without an instance use the HBM-streaming CSR decoder
 // (bp_exact.cu).
 //   1,384 : config 2        1,192 : configs 3 and 4       2,26 : config 1
+//   1,64 / 2,64 / 2,384 : config 5's decoder-only geometries
 #define LSB_QCX_INSTANCES(V) \
   V(1, 384, 2)               \
   V(1, 192, 2)               \
+  V(1, 64, 2)                \
+  V(2, 384, 2)               \
+  V(2, 64, 2)                \
   V(2, 26, 2)

@@ -47,7 +47,7 @@ def _check_mother(code, oc, mother, variant, es, num_iter=20):
 
 
 @pytest.mark.parametrize("k,n,m,ebno", [(256, 512, 2, 2.5), (8448, 16896, 4, 5.2), (4096, 8192, 2, 1.5),
-                                        (4096, 12288, 6, 7.0)])
+                                        (4096, 12288, 6, 7.0), (1408, 2816, 2, 2.5)])
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("es", [True, False])
 def test_qc_exact_mother_input_bit_exact(k, n, m, ebno, variant, es):
