@@ -306,7 +306,7 @@ def run_b200(a, rank, world, local_rank):
         line["fast_fp32_full_graph"] = fast_rate(a, rank, world, dist, "fp32-full", prune=False)
         line["sum_product_fast"] = sum_product_rate(a, rank, world, dist)
         if rank == 0:
-            line["sum_product_f32_config3"] = sum_product_f32_rate(a)
+            line["sum_product_f32"] = sum_product_f32_rate(a)
         line["config3_sweep"] = config3_sweep(a, rank, world, dist)
         line["config4_demappers"] = config4_demappers(a, rank, world, dist)
         if rank == 0:
@@ -587,18 +587,15 @@ def config5_decoder_only(a):
                                   "Z >= 32 is the harness-lifted graph (LdpcCode5G(k, n, base_graph=2, z=Z))"}
 
 
-def sum_product_f32_rate(a, B=32768):
-    """The f32-message sum-product option (k_qc_sp32, within 1e-4 of exact
-    sum-product on converged codewords) next to the fp16-message kernel, on
-    config 3 (BG1 k=4096 r=1/2, Z=192: where f32 messages fit on chip)."""
+def _sp_rates(a, k, n, m, ebno, B):
     import torch
 
     import paper_2203_11854_b200 as lb
 
     pipe = lb.Pipeline(lb.SimConfig.from_dict({
-        "code": {"family": "ldpc5g", "k": 4096, "n": 8192, "decoder": {"mode": "fast"}},
-        "modulation": {"kind": "qam", "bits_per_symbol": 2}, "sweep": {"ebno_db": [2.0], "batch_size": B}}))
-    payload, llr = pipe._llr(2.0, B, lb.RngStream(a.seed, 31))
+        "code": {"family": "ldpc5g", "k": k, "n": n, "decoder": {"mode": "fast"}},
+        "modulation": {"kind": "qam", "bits_per_symbol": m}, "sweep": {"ebno_db": [ebno], "batch_size": B}}))
+    payload, llr = pipe._llr(ebno, B, lb.RngStream(a.seed, 31))
     out = {}
     for prec in ("fp32-full", "fp32"):
         def run():
@@ -613,9 +610,20 @@ def sum_product_f32_rate(a, B=32768):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         out["f32_messages" if prec == "fp32-full" else "fp16_messages"] = {
-            "ms": ms, "gbit_s": B * 4096 / (ms / 1e3) / 1e9}
-    out["note"] = ("decoder only, 20 fixed iterations, 2.0 dB; f32 messages: k_qc_sp32 (3 MUFU per edge, "
-                   "division-free product domain with prefix/suffix products); fp16 messages: k_qc_sp (4 MUFU, product domain)")
+            "ms": ms, "gbit_s": B * k / (ms / 1e3) / 1e9}
+    return out
+
+
+def sum_product_f32_rate(a, B=32768):
+    """The f32-message sum-product option (k_qc_sp32, within 1e-4 of exact
+    sum-product on converged codewords) next to the fp16-message kernel, on
+    config 3 (BG1 k=4096 r=1/2, Z=192: f32 messages in shared memory) and
+    config 2 (Z=384: f32 messages in an L2 slice per CTA)."""
+    out = _sp_rates(a, 4096, 8192, 2, 2.0, B)
+    out["config2"] = _sp_rates(a, K_INFO, N_TX, M_BITS, 4.8, B // 2)
+    out["note"] = ("decoder only, 20 fixed iterations, config 3 at 2.0 dB (config2: 4.8 dB); f32 messages: "
+                   "k_qc_sp32 (3 MUFU per edge, division-free product domain with prefix/suffix products; "
+                   "config 2: messages in L2); fp16 messages: k_qc_sp (4 MUFU, product domain)")
     return out
 
 

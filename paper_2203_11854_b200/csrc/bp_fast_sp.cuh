@@ -434,23 +434,27 @@ struct Sp32Tab {
   }
 };
 
-template <class G, int Z, int R, int SPLIT, bool ES>
+// GM: the f32 messages do not fit in shared memory with the posteriors
+// (config 2: 344 KB); they live in an L2-resident slice per CTA and the
+// CTAs loop over the batch (persistent grid)
+template <class G, int Z, int R, int SPLIT, bool ES, bool GM>
 __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z, R, SPLIT>::MINB)
-    k_qc_sp32(const QcChanParams P, const Sp32Tab<G, Z, R> tab, const float *__restrict__ llr, int num_iter,
-              uint8_t *__restrict__ hard_k, float *__restrict__ llr_out, int32_t *__restrict__ iters_used,
-              const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts) {
+    k_qc_sp32(const QcChanParams P, const Sp32Tab<G, Z, R> tab, const float *__restrict__ llr, int64_t batch,
+              int num_iter, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
+              int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts,
+              float *__restrict__ c2vws) {
   using S = QcShapeSP<G, Z, R, SPLIT>;
   using Tab = Sp32Tab<G, Z, R>;
   constexpr int NT = S::NT, NT1 = S::NT1, NCOLZ = S::NCOL * Z;
   extern __shared__ float smf[];
-  float *c2v = smf;                     // [NE][Z]
-  float *tot = smf + (size_t)S::NE * Z;  // [NCOL][Z]
+  float *c2v = GM ? c2vws + (size_t)blockIdx.x * S::NE * Z : smf;  // [NE][Z]
+  float *tot = GM ? smf : smf + (size_t)S::NE * Z;                   // [NCOL][Z]
   const char *const totb = reinterpret_cast<const char *>(tot);
   const int t = threadIdx.x;
   const int h = t / NT1;  // thread group: every SPLIT-th row / column of each degree class
   const int i = t - h * NT1;
   const bool lane = NT1 == Z || i < Z;
-  const int64_t b = blockIdx.x;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
   const float *row = llr + b * (int64_t)P.n;
 
   for (int v = t; v < NCOLZ; v += NT) tot[v] = chan_value(P, row, v) * kLog2e;
@@ -587,6 +591,8 @@ __global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z,
       }
     }
   }
+  __syncthreads();
+  }
 }
 
 template <class G, int Z, int R, int SPLIT>
@@ -596,21 +602,38 @@ int launch_qc_sp32(const QcChanParams &P, const float *llr, int64_t B, int num_i
   (void)alpha;
   using S = QcShapeSP<G, Z, R, SPLIT>;
   using Tab = Sp32Tab<G, Z, R>;
-  static_assert(sizeof(Tab) + sizeof(QcChanParams) + 96 <= 32000, "kernel parameters too large");
-  constexpr size_t smem = 2 * S::SMEM;  // f32 messages and posteriors
-  static_assert(smem <= 227 * 1024, "f32 sum-product messages do not fit in shared memory");
+  static_assert(sizeof(Tab) + sizeof(QcChanParams) + 128 <= 32000, "kernel parameters too large");
+  // f32 messages and posteriors in shared memory, or the messages in L2
+  constexpr bool GM = 2 * S::SMEM > 227 * 1024;
+  constexpr size_t smem = GM ? 4ull * S::NCOL * Z : 2 * S::SMEM;
+  static_assert(smem <= 227 * 1024, "f32 sum-product posteriors do not fit in shared memory");
   static constexpr Tab tab{};
-  auto kern = early_stop ? k_qc_sp32<G, Z, R, SPLIT, true> : k_qc_sp32<G, Z, R, SPLIT, false>;
+  auto kern = early_stop ? k_qc_sp32<G, Z, R, SPLIT, true, GM> : k_qc_sp32<G, Z, R, SPLIT, false, GM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(smem attr)");
+  if (B <= 0) return LS_OK;
+  float *ws = nullptr;
+  int64_t grid = B;
+  if (GM) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::NT, smem);
+    grid = std::min<int64_t>((int64_t)sms * std::max(1, per_sm), B);
+    retain_pool_memory();
+    e = cudaMallocAsync((void **)&ws, sizeof(float) * (size_t)grid * S::NE * Z, s);
+    if (e != cudaSuccess) return cuda_status(e, "ls_qc_decode(sp32 message workspace)");
+  }
   for (int64_t b0 = 0; b0 < B; b0 += 0x7fffffff) {
     const int64_t nb = B - b0 < 0x7fffffff ? B - b0 : 0x7fffffff;
-    kern<<<(unsigned)nb, S::NT, smem, s>>>(P, tab, llr + b0 * P.n, num_iter, hard_k ? hard_k + b0 * P.k : nullptr,
-                                            llr_out ? llr_out + b0 * P.n_full : nullptr,
-                                            iters_used ? iters_used + b0 : nullptr, ref ? ref + b0 * P.k : nullptr,
-                                            counts);
+    const int64_t g = std::min<int64_t>(grid, nb);
+    kern<<<(unsigned)g, S::NT, smem, s>>>(P, tab, llr + b0 * P.n, nb, num_iter, hard_k ? hard_k + b0 * P.k : nullptr,
+                                          llr_out ? llr_out + b0 * P.n_full : nullptr,
+                                          iters_used ? iters_used + b0 : nullptr, ref ? ref + b0 * P.k : nullptr,
+                                          counts, ws);
   }
   e = cudaGetLastError();
+  if (ws) cudaFreeAsync(ws, s);
   return e == cudaSuccess ? LS_OK : cuda_status(e, "ls_qc_decode");
 }
 

@@ -11,8 +11,8 @@
 //                         1/2 and BG2 rate 1/3 lifted at any Z, fp16x2)
 // kind f32: k_qc_fast2 (bp_fast_qc.cuh); h2: k_qc_fast_h2 (bp_fast_h2.cuh);
 // sp: k_qc_sp, sum-product (bp_fast_sp.cuh); sp32: k_qc_sp32, sum-product with
-// f32 messages and the log-domain check update (accuracy option, where the
-// messages fit in shared memory)
+// f32 messages and the product-domain check update (accuracy option; at
+// Z = 384 the messages live in an L2 slice per CTA)
 #pragma once
 #define LSB_QC_INSTANCES(X) \
   X(1, 384, 24, 2, f32)     \
@@ -45,6 +45,7 @@
   X(1, 192, 46, 2, sp)      \
   X(2, 26, 12, 1, sp)       \
   X(2, 26, 42, 1, sp)       \
+  X(1, 384, 24, 1, sp32)    \
   X(1, 192, 24, 2, sp32)    \
   X(2, 26, 12, 1, sp32)     \
   X(2, 26, 42, 1, sp32)

@@ -229,10 +229,11 @@ def test_fp32_full_graph_noiseless_and_fixed_iterations():
 
 
 @pytest.mark.parametrize("k,n,m,ebno", [(4096, 8192, 2, 1.75), (4096, 8192, 2, 2.25), (256, 512, 2, 2.0),
-                                        (256, 512, 2, 3.0)])
+                                        (256, 512, 2, 3.0), (8448, 16896, 4, 4.6)])
 def test_sum_product_f32_messages_close_to_exact(k, n, m, ebno):
-    """The f32-message sum-product option (k_qc_sp32: log-domain check update
-    with prefix/suffix exclusive sums, the reference's f32 first pass) against
+    """The f32-message sum-product option (k_qc_sp32: product-domain check
+    update with prefix/suffix products, the reference's f32 first pass; at
+    config 2 the messages live in an L2 slice per CTA) against
     the exact sum-product decoder (CSR engine, the reference's arithmetic): on
     the codewords both converge on at the same iteration, identical hard
     decisions and >= 99.9 % of the mother LLRs within 1e-4 * max(|L|, 1) (the
@@ -240,7 +241,7 @@ def test_sum_product_f32_messages_close_to_exact(k, n, m, ebno):
     code = lb.LdpcCode5G(k, n)
     oc = O.code(k, n)
     assert LD.qc_has_kernel(code, precision="fp32-full", variant="sum-product")
-    B = 192 if k > 1000 else 400
+    B = 96 if k > 8000 else (192 if k > 1000 else 400)
     _, llr = _llrs(k, n, m, ebno, B, 44)
     mother = oc.derate_match(llr)
     lo_e, hard_e, it_e = lb.bp_decode(mother, code.pcm, 20, "sum-product", 0.75, True, return_iters=True,
@@ -258,8 +259,8 @@ def test_sum_product_f32_messages_close_to_exact(k, n, m, ebno):
     assert np.array_equal(r["hard"].cpu().numpy()[conv], hard_e[conv][:, :k])
 
 
-def test_sum_product_f32_messages_unavailable_where_they_do_not_fit():
-    code = lb.LdpcCode5G(8448, 16896)
+def test_sum_product_f32_messages_unavailable_without_an_instance():
+    code = lb.LdpcCode5G(1408, 2816)  # BG1 Z=64: no f32-message sum-product instance
     assert not LD.qc_has_kernel(code, precision="fp32-full", variant="sum-product")
     with pytest.raises(ValueError):
         LD.qc_decode(np.zeros((2, code.n), np.float32), code, 5, "sum-product", precision="fp32-full")
