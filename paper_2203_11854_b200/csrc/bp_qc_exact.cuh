@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         }
         if (cw >= 0) {
           // zero check state: the first iteration's old messages are +0
-          if constexpr (!ES) sfor<0, MB>([&](auto rc) {
+          if constexpr (!(ES && NC == 1)) sfor<0, MB>([&](auto rc) {
             constexpr int r = decltype(rc)::value;
             if (grp != Geo::rowner(r)) return;
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
@@ -379,12 +379,13 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         constexpr int e0 = G::row_start[r], D = Geo::deg(r);
         using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
         WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
-        // old messages are +0 in the first iteration: fixed-iteration kernels
-        // zero a refilled slot's state (no branch in the hot loop), early-stop
-        // ones skip the loads (a different register allocation wins there)
+        // old messages are +0 in the first iteration: a refilled slot's state
+        // is zeroed (no branch in the hot loop, slots stay in step), except
+        // for one-slot early-stop kernels, which skip the loads (a different
+        // register allocation wins there)
         M m1o = 0, m2o = 0;
         uint32_t wo = 0u;
-        if (!ES || !first) {
+        if (!(ES && NC == 1) || !first) {
           m1o = M1l[r * NZ];
           m2o = m2l[r * NZ];
           wo = (uint32_t)W[ln];
