@@ -169,6 +169,24 @@ def test_qc_exact_codeword_slots_equal_csr_engine(k, n, m, ebno, B):
         assert [int(x) for x in r["counts"].cpu()] == [be, ble]
 
 
+@pytest.mark.parametrize("k,n", [(256, 512), (8448, 16896), (1408, 2816)])
+@pytest.mark.parametrize("num_iter", [1, 2, 3])
+def test_qc_exact_few_iterations_equal_csr_engine(k, n, num_iter):
+    """1-3 iterations (the first iteration has no early-stop test; zeroed
+    slot state must equal the reference's zero messages), with and without
+    early stop, one slot (Z=384) and several (Z=26: 14, Z=64: 6)."""
+    code = lb.LdpcCode5G(k, n)
+    oc = O.code(k, n)
+    _, llr = _llrs(k, n, 2, 3.0, 300 if k < 1000 else 64, 17)
+    mother = oc.derate_match(llr)
+    for es in (True, False):
+        a = lb.bp_decode(mother, code.pcm, num_iter, "scaled-min-sum", 0.75, es, return_iters=True, engine="qc")
+        b = lb.bp_decode(mother, code.pcm, num_iter, "scaled-min-sum", 0.75, es, return_iters=True, engine="csr")
+        assert np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+        assert np.array_equal(a[1], b[1])
+        assert np.array_equal(a[2], b[2])
+
+
 def test_qc_exact_rejects_sum_product_and_unknown_engine():
     code = lb.LdpcCode5G(256, 512)
     llr = np.zeros((2, code.n_full), np.float32)
