@@ -438,7 +438,7 @@ struct Sp32Tab {
 // (config 2: 344 KB); they live in an L2-resident slice per CTA and the
 // CTAs loop over the batch (persistent grid)
 template <class G, int Z, int R, int SPLIT, bool ES, bool GM>
-__global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, QcShapeSP<G, Z, R, SPLIT>::MINB)
+__global__ void __launch_bounds__(QcShapeSP<G, Z, R, SPLIT>::NT, GM ? 2 : QcShapeSP<G, Z, R, SPLIT>::MINB)
     k_qc_sp32(const QcChanParams P, const Sp32Tab<G, Z, R> tab, const float *__restrict__ llr, int64_t batch,
               int num_iter, uint8_t *__restrict__ hard_k, float *__restrict__ llr_out,
               int32_t *__restrict__ iters_used, const uint8_t *__restrict__ ref, unsigned long long *__restrict__ counts,

@@ -1,4 +1,7 @@
-import sys, torch; sys.path.insert(0, "/root/repo")
+import os, sys, torch; sys.path.insert(0, "/root/repo")
+if len(sys.argv) > 1:
+    from paper_2203_11854_b200 import _lib
+    _lib.LIB_PATH = os.path.abspath(sys.argv[1])
 import paper_2203_11854_b200 as lb
 B = 8192
 pipe = lb.Pipeline(lb.SimConfig.from_dict({"code": {"family": "ldpc5g", "k": 8448, "n": 16896, "decoder": {"mode": "fast"}},
