@@ -7,7 +7,7 @@ driven by Pipeline.run_batch / run_sweep.  All array work runs in the CUDA
 library liblinksim_b200.so (include/linksim_b200.h); there is no CPU
 fallback.
 """
-from .alist import ParityCheckMatrix
+from .alist import AlistParseError, ParityCheckMatrix, parse_alist, to_alist
 from .channel import awgn, complex_gaussian
 from .core import (LLR_MAX, RngStream, binary_source, compute_ber, compute_bler, count_errors,
                    ebnodb2no, hard_decide)
@@ -19,7 +19,7 @@ from .sweep import (ConfigError, Pipeline, SimConfig, SnrPointResult, SweepResul
 
 __version__ = "0.1.0"
 __all__ = [
-    "ParityCheckMatrix", "awgn", "complex_gaussian", "LLR_MAX", "RngStream", "binary_source",
+    "ParityCheckMatrix", "AlistParseError", "parse_alist", "to_alist", "awgn", "complex_gaussian", "LLR_MAX", "RngStream", "binary_source",
     "compute_ber", "compute_bler", "count_errors", "ebnodb2no", "hard_decide", "BP_VARIANTS",
     "LIFTING_SIZES", "LdpcCode5G", "bp_decode", "exit_mutual_information", "ldpc5g_decode",
     "ldpc5g_encode", "qc_decode", "Constellation", "demap_app", "demap_maxlog", "map_bits",
