@@ -42,3 +42,20 @@ def test_exit_tracking_demo_trajectory(ebno_db):
         if ebno_db >= 1.0:
             assert mi >= prev - 1e-3  # the climb toward 1.0 above threshold
         prev = mi
+
+
+def test_waterfall_demo_sweep_matches_reference():
+    """demos/ldpc_waterfall.py (the Listing-1 sweep: k=500 n=1000 sum-product,
+    16-QAM max-log, 3-7 dB, error-count stop) through this package's
+    run_sweep in exact mode, against the reference's own run_sweep result
+    (tests/golden/demo_waterfall.json, tests/golden/make_demo_golden.py)."""
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "demo_waterfall.json")))
+    res = lb.run_sweep(lb.SimConfig.from_dict(gold["config"]), num_workers=4)
+    assert len(res.points) == len(gold["points"])
+    for p, g in zip(res.points, gold["points"]):
+        assert (p.ebno_db, p.bits, p.blocks, p.batches, p.stop_reason) == (
+            g["ebno_db"], g["bits"], g["blocks"], g["batches"], g["stop_reason"])
+        assert (p.bit_errors, p.block_errors) == (g["bit_errors"], g["block_errors"])
