@@ -110,13 +110,19 @@ struct QxGeo {
 
   // contiguous degree-balanced ranges: rows [rfirst(g), rfirst(g+1)) and
   // core columns [cfirst(g), cfirst(g+1)) belong to thread group g
-  static constexpr int rfirst(int g) {
+  // `shift` moves the group boundaries down the row list: the early-stop
+  // kernels' extension rows cost more than their edge count says (syndrome
+  // and extension posterior): measured best with the boundary 4 rows later
+  // (early stop at 6 dB, Z = 384: 14.18 -> 13.32 ms per 8,192; Z = 192 at
+  // 3 dB: 20.15 -> 19.43 ms per 16,384; the fixed-iteration kernels keep 0)
+  static constexpr int rfirst(int g, int shift = 0) {
     if (g <= 0) return 0;
     if (g >= NTL) return MB;
     const int tot = G::row_start[MB];
     int r = 0;
     while (r < MB && G::row_start[r] * NTL < tot * g) ++r;
-    return r;
+    r += shift;
+    return r < MB ? r : MB;
   }
   // variable-node work of core column c in instructions (~13 per edge plus
   // the per-column channel load, sum and store), for balancing the groups
@@ -132,9 +138,9 @@ struct QxGeo {
   }
   // thread group owning row r / core column c (compile-time only: the
   // tables are host constexpr arrays)
-  static constexpr int rowner(int r) {
+  static constexpr int rowner(int r, int shift = 0) {
     int g = 0;
-    while (g + 1 < NTL && r >= rfirst(g + 1)) ++g;
+    while (g + 1 < NTL && r >= rfirst(g + 1, shift)) ++g;
     return g;
   }
   static constexpr int cowner(int c) {
@@ -262,6 +268,10 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
   using M = typename Geo::M;
   constexpr int Z = Geo::Z, NZ = Geo::NZ, NC = Geo::NC, NT1 = Geo::NT1, NTL = Geo::NTL, MB = Geo::MB;
   constexpr int KBC = Geo::KBC, SLOT_T = NTL * Z;  // threads per slot
+#ifndef QX_ES_ROW_SHIFT
+#define QX_ES_ROW_SHIFT 4
+#endif
+  constexpr int RSH = ES ? QX_ES_ROW_SHIFT : 0;  // row split of the thread groups (rfirst)
   extern __shared__ __align__(16) unsigned char qx_sm[];
   M *M1 = reinterpret_cast<M *>(qx_sm);
   // min2 per check: an L2 slice per CTA for f64 messages, shared memory for f32
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
           // zero check state: the first iteration's old messages are +0
           if constexpr (!(ES && NC == 1)) sfor<0, MB>([&](auto rc) {
             constexpr int r = decltype(rc)::value;
-            if (grp != Geo::rowner(r)) return;
+            if (grp != Geo::rowner(r, RSH)) return;
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
             M1l[r * NZ] = (M)0;
             m2l[r * NZ] = (M)0;
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       const char *Tk = reinterpret_cast<const char *>(T) + k4;
       sfor<0, MB>([&](auto rc) {
         constexpr int r = decltype(rc)::value;
-        if (grp != Geo::rowner(r)) return;  // warp-uniform
+        if (grp != Geo::rowner(r, RSH)) return;  // warp-uniform
         constexpr int e0 = G::row_start[r], D = Geo::deg(r);
         using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
         WT *W = reinterpret_cast<WT *>(qx_sm + Geo::woff(r));
@@ -482,7 +492,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
       if (fin && used == num_iter) {
         sfor<4, MB>([&](auto rc) {
           constexpr int r = decltype(rc)::value;
-          if (grp != Geo::rowner(r)) return;
+          if (grp != Geo::rowner(r, RSH)) return;
           constexpr int D = Geo::deg(r), e = G::row_start[r + 1] - 1, c = G::col[e], s = G::shift[e] % Z;
           if constexpr (c >= KBC) {
             using WT = std::conditional_t<Geo::wbytes(r) == 4, uint32_t, uint16_t>;
