@@ -66,6 +66,9 @@ namespace lsb {
 // Z = 192 per CTA left half the warps per row and stalled on instruction
 // fetch, profiles/r02/README.md).
 constexpr int qx_default_nc(int z) { return z >= 384 ? 1 : 384 / z; }
+#ifndef QX_COL_SHIFT
+#define QX_COL_SHIFT -1  // variable-phase column split offset (QxGeo::cfirst)
+#endif
 
 template <class G_, int Z_, int NTL_, class M_ = double, int NC_ = qx_default_nc(Z_)>
 struct QxGeo {
@@ -134,7 +137,10 @@ struct QxGeo {
     for (int c = 0; c < KBC; ++c) tot += ccost(c);
     int c = 0, acc = 0;
     while (c < KBC && acc * NTL < tot * g) acc += ccost(c++);
-    return c;
+    // one column earlier than the cost model says: measured 29.29 -> 29.18 ms
+    // (Z = 384, fixed) and 13.30 -> 13.25 ms (early stop); 0, +1, -2, -3 are slower
+    c += QX_COL_SHIFT;
+    return c > 0 ? c : 0;
   }
   // thread group owning row r / core column c (compile-time only: the
   // tables are host constexpr arrays)
@@ -271,7 +277,10 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
 #ifndef QX_ES_ROW_SHIFT
 #define QX_ES_ROW_SHIFT 4
 #endif
-  constexpr int RSH = ES ? QX_ES_ROW_SHIFT : 0;  // row split of the thread groups (rfirst)
+#ifndef QX_FX_ROW_SHIFT
+#define QX_FX_ROW_SHIFT 0
+#endif
+  constexpr int RSH = ES ? QX_ES_ROW_SHIFT : QX_FX_ROW_SHIFT;  // row split of the thread groups (rfirst)
   extern __shared__ __align__(16) unsigned char qx_sm[];
   M *M1 = reinterpret_cast<M *>(qx_sm);
   // min2 per check: an L2 slice per CTA for f64 messages, shared memory for f32
