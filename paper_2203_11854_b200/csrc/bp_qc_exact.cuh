@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         if (nx >= 0) {
           const char *nrow = reinterpret_cast<const char *>(llr + nx * (int64_t)row_len);
           for (int b = 128 * ts; b < 4 * row_len; b += 128 * SLOT_T) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + b));
-          if (!ES && ref && 128 * ts < P.k)  // and its reference bits (one line per thread)
+          if (ref && 128 * ts < P.k)  // and its reference bits (one line per thread)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ref + nx * (int64_t)P.k + 128 * ts));
         }
         if (cw >= 0) {
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(Geo::NT, Geo::MINB)
         for (int v = ts; v < P.n_full; v += SLOT_T) o[v] = -post(v);
       }
       unsigned err = 0;
-      if (!ES && !hard && ref && (P.k & 3) == 0) {
+      if (!hard && ref && (P.k & 3) == 0) {
         // error count only: the reference bits four at a time
         const uint32_t *rw = reinterpret_cast<const uint32_t *>(ref + cw * (int64_t)P.k);
         for (int w = ts; w < (P.k >> 2); w += SLOT_T) {
